@@ -1,0 +1,186 @@
+/*
+ * dcnn.h -- C ABI of the B200-native DeltaCNN engine (libdcnn.so).
+ *
+ * The library implements frame-to-frame delta propagation through a CNN
+ * (DeltaCNN, arXiv 2203.03996, §3.1 "Delta value propagation",
+ * Eqs. 1-6, Fig. 2): "a stream of frames in, dense-equivalent outputs out".
+ * Each call advances S independent camera streams (the paper's
+ * batch dimension) by one frame on one GPU.
+ *
+ * Conventions (all entry points):
+ *   - Layout: NHWC everywhere (S1.3).  Frames [S,H,W,C],
+ *     outputs [S,Ho,Wo,Co]; weights OHWI [C_out][kh][kw][C_in/groups]
+ *     (SPEC.md S:113 order).
+ *   - Ownership: the caller owns frame and output buffers.  The library copies
+ *     weights/biases at create time and owns every cache, mask, work list and
+ *     CUDA graph.  Nothing the caller passes is retained after a call returns.
+ *   - Errors: status codes only; no exceptions cross the ABI.  Argument and
+ *     shape errors are synchronous.  Device-detected errors (non-finite input
+ *     frame values) are sticky: they are reported as DCNN_ERR_NONFINITE by the
+ *     next dcnn_process_frame / dcnn_get_stats call on that net.  A thread-local
+ *     message is available from dcnn_last_error().
+ *   - Threading: a net is externally synchronised; different
+ *     nets may be used from different threads.
+ *   - Stream order: process_frame enqueues on the given cudaStream_t and returns
+ *     without synchronising; results are valid when that stream reaches the
+ *     end of the enqueued work.  Only dcnn_get_stats / dcnn_debug_read (and the
+ *     _host variant of process_frame) synchronise.
+ *   - Unsupported op/parameter combinations fail at create
+ *     (DCNN_ERR_UNSUPPORTED), never at run time.
+ */
+#ifndef DCNN_H
+#define DCNN_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DCNN_API __attribute__((visibility("default")))
+#else
+#define DCNN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dcnn_net dcnn_net;   /* opaque */
+
+typedef enum {
+  DCNN_OK = 0,
+  DCNN_ERR_ARG = 1,          /* null pointer, out-of-range index, bad enum      */
+  DCNN_ERR_SHAPE = 2,        /* inconsistent shapes / dangling layer reference  */
+  DCNN_ERR_UNSUPPORTED = 3,  /* op / parameter combination not implemented     */
+  DCNN_ERR_NONFINITE = 4,    /* sticky: a non-finite input value was seen       */
+  DCNN_ERR_CUDA = 5,         /* CUDA runtime error (message in dcnn_last_error) */
+  DCNN_ERR_OOM = 6           /* device allocation failed                        */
+} dcnn_status;
+
+typedef enum { DCNN_F32 = 0, DCNN_F16 = 1 } dcnn_dtype;
+
+/* Op kinds (§3.4 "convolutions, batch normalizations, pooling
+ * layers, upsampling layers, activations, concatenations and additions"). */
+typedef enum {
+  DCNN_OP_CONV = 0,              /* delta conv, Eq. 1; bias on the first frame only */
+  DCNN_OP_ACT = 1,               /* activation + truncation, Eqs. 4-6                          */
+  DCNN_OP_MAXPOOL = 2,           /* Eq. 3 with f = max-pool over the accumulated input          */
+  DCNN_OP_AVGPOOL = 3,           /* linear; divide by kh*kw (zero padding counted)             */
+  DCNN_OP_UPSAMPLE_NEAREST = 4,  /* replicate delta and mask                                    */
+  DCNN_OP_ADD = 5,               /* mask union, absent operand = 0; optional fused act+trunc    */
+  DCNN_OP_CONCAT = 6,            /* channel concat, mask union, zero-filled inactive operands   */
+  DCNN_OP_AFFINE = 7             /* unfolded BN: dy = scale*dx (+shift on the first frame)      */
+} dcnn_op;
+
+/* Activation f of Eq. 5.  act != NONE makes the op a truncation point
+ * ("combining activation and truncation into a single operation"). */
+typedef enum {
+  DCNN_ACT_NONE = 0, DCNN_ACT_RELU = 1, DCNN_ACT_SILU = 2, DCNN_ACT_RELU6 = 3,
+  DCNN_ACT_LEAKY = 4, DCNN_ACT_SIGMOID = 5
+} dcnn_act;
+
+typedef struct {
+  int32_t op;              /* dcnn_op                                                    */
+  int32_t n_in;            /* 1..4 (ADD / CONCAT), 1 otherwise                           */
+  int32_t in[4];           /* producer op indices (< own index); -1 = network input      */
+  int32_t c_out;           /* CONV: output channels                                      */
+  int32_t kh, kw;          /* CONV / pools: window                                       */
+  int32_t stride, pad, dilation, groups;
+  int32_t up_factor;       /* UPSAMPLE_NEAREST                                           */
+  int32_t act;             /* dcnn_act (CONV, ACT, ADD)                                  */
+  float act_param;         /* LEAKY slope (0 -> 0.1)                                      */
+  float threshold;         /* eps of Eqs. 4-6: updated iff max_c|dy_c| > eps (strict);
+                              eps < 0 never truncates (dense mode)          */
+  const float* weight;     /* CONV: host fp32 OHWI, copied (and cast) at create          */
+  const float* bias;       /* CONV: host fp32 [c_out] or NULL                            */
+  const float* scale;      /* AFFINE: host fp32 [C]                                      */
+  const float* shift;      /* AFFINE: host fp32 [C]                                      */
+} dcnn_layer_desc;
+
+enum {
+  DCNN_FLAG_NO_TENSOR_CORES = 1   /* route every conv through the CUDA-core kernel      */
+};
+
+typedef struct {
+  int32_t in_h, in_w, in_c;       /* frame shape per stream                                  */
+  int32_t n_streams;              /* S: streams advanced together by one process_frame call */
+  int32_t device;                 /* CUDA device ordinal                                     */
+  int32_t dtype;                  /* dcnn_dtype of frames, deltas, caches and weights;
+                                     accumulation is fp32, outputs fp32  */
+  float input_threshold;          /* eps_in; < 0: every pixel active          */
+  int32_t input_dilation;         /* Chebyshev radius r of the input-mask dilation  */
+  int32_t n_layers;
+  const dcnn_layer_desc* layers;  /* topological order                                       */
+  int32_t n_outputs;
+  const int32_t* output_ops;      /* ops whose dense accumulated output O is returned */
+  int32_t flags;                  /* DCNN_FLAG_*                                              */
+} dcnn_net_desc;
+
+/* Per-op counters of the most recent frame, summed over streams (SPEC.md
+ * S:369-374 RunStats).  Index 0 of the array is the input layer, index i+1 op i. */
+typedef struct {
+  int64_t active_in;       /* active input pixels (first input for multi-input ops)   */
+  int64_t active_out;      /* active output pixels after truncation                   */
+  int64_t tiles_total;     /* CONV: output tiles                                      */
+  int64_t tiles_skip;      /* CONV: tiles with no active input         */
+  int64_t tiles_sparse;    /* CONV: tiles run on the CUDA-core path                   */
+  int64_t tiles_dense;     /* CONV: tiles run on the tensor-core path                 */
+  int64_t mac_alg;         /* CONV: kh*kw*C_in/g*C_out MACs per pre-truncation active
+                              output pixel                                            */
+  int64_t mac_exec;        /* CONV: MACs executed incl. tile waste                    */
+} dcnn_op_stats;
+
+enum { DCNN_BUF_DELTA = 0, DCNN_BUF_MASK = 1, DCNN_BUF_XA = 2, DCNN_BUF_XT = 3,
+       DCNN_BUF_OUT = 4, DCNN_BUF_POOLA = 5 };
+
+/* Build a net: validates the description, infers shapes, copies weights
+ * (cast to dtype), allocates all device state and plans tiles.  The next
+ * process_frame of every stream is a dense first frame. */
+DCNN_API dcnn_status dcnn_create_net(const dcnn_net_desc* desc, dcnn_net** out);
+
+/* Set eps of op (0..n_layers-1, must have act != NONE) or of the input layer
+ * (op = -1).  Takes effect from the next enqueued frame; no re-planning. */
+DCNN_API dcnn_status dcnn_set_threshold(dcnn_net* net, int32_t op, float eps);
+
+/* Advance every stream by one frame.
+ *   frames  : device pointer, [S,in_h,in_w,in_c] in desc.dtype, NHWC.
+ *   outputs : array of n_outputs device pointers, each [S,Ho,Wo,Co] fp32;
+ *             receives the dense accumulated output O^i.
+ *             May be NULL (outputs stay readable through DCNN_BUF_OUT).
+ *   stream  : cudaStream_t (as void*); 0 = legacy default stream. */
+DCNN_API dcnn_status dcnn_process_frame(dcnn_net* net, const void* frames, void* const* outputs,
+                               void* stream);
+
+/* Same with HOST buffers: copies frames host->device, runs, copies outputs
+ * device->host, and synchronises the stream before returning. */
+DCNN_API dcnn_status dcnn_process_frame_host(dcnn_net* net, const void* host_frames,
+                                    void* const* host_outputs, void* stream);
+
+/* Flush the caches of one stream (or all with -1): its next frame is dense
+ * again (PAPER.md:715-719 S1.4).  Ordered after work previously enqueued by
+ * process_frame on this net. */
+DCNN_API dcnn_status dcnn_reset(dcnn_net* net, int32_t stream);
+
+DCNN_API void dcnn_destroy_net(dcnn_net* net);
+
+/* Shapes of op (or -1 = input layer): H, W, C of its output.  No sync. */
+DCNN_API dcnn_status dcnn_op_shape(dcnn_net* net, int32_t op, int32_t* H, int32_t* W, int32_t* C);
+
+/* Copies counters of the last frame (array of n_layers+1 entries), the frame
+ * index of stream 0 and the sticky device error.  Synchronises the device. */
+DCNN_API dcnn_status dcnn_get_stats(dcnn_net* net, dcnn_op_stats* per_op, int64_t* frame_index,
+                           int32_t* device_error);
+
+/* Copy one internal buffer of op (-1 = input layer) to host memory (all streams):
+ * DELTA/XA/XT/POOLA in dtype, MASK u8, OUT fp32.  Synchronises the device.
+ * bytes receives the buffer size; host may be NULL to query the size only. */
+DCNN_API dcnn_status dcnn_debug_read(dcnn_net* net, int32_t op, int32_t which, void* host,
+                            int64_t* bytes);
+
+/* Number of kernel launches enqueued by one process_frame (graph nodes). */
+DCNN_API int32_t dcnn_kernels_per_frame(dcnn_net* net);
+
+DCNN_API const char* dcnn_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DCNN_H */

@@ -1,0 +1,618 @@
+// dcnn.cu -- host runtime of libdcnn.so: the C ABI of include/dcnn.h.
+//
+// create: validate + shape inference + weight copy/cast + device state + plan.
+// process_frame: one CUDA-graph launch per frame (captured on first use); every
+// per-layer work count lives on the device, so there is no host sync per frame.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dcnn.h"
+#include "kernels.h"
+
+using namespace dcnn;
+
+static thread_local std::string g_err;
+
+static dcnn_status fail(dcnn_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(x)                                                                     \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) {                                                            \
+      return fail(e_ == cudaErrorMemoryAllocation ? DCNN_ERR_OOM : DCNN_ERR_CUDA,       \
+                  std::string(#x) + ": " + cudaGetErrorString(e_));                     \
+    }                                                                                   \
+  } while (0)
+
+namespace {
+
+struct Op {
+  int kind = 0, n_in = 1, in[4] = {-1, -1, -1, -1};
+  int H = 0, W = 0, C = 0;          // output shape
+  int Hi = 0, Wi = 0, Ci = 0;       // shape of input 0
+  int Cin[4] = {0, 0, 0, 0};
+  int kh = 1, kw = 1, stride = 1, pad = 0, dil = 1, groups = 1, up = 1;
+  int act = 0;
+  float act_param = 0.1f;
+  // device buffers
+  void* delta = nullptr;
+  uint8_t* mask = nullptr;
+  void* xA = nullptr;
+  void* xT = nullptr;
+  void* poolA = nullptr;
+  float* O = nullptr;
+  int out_slot = -1;
+  // conv
+  float* wt = nullptr;
+  float* bias = nullptr;
+  int Cp = 0, K = 0;
+  int TH = 8, TW = 8, nty = 0, ntx = 0, STH = 8, STW = 8, WH = 0, WW = 0, CIC = 0, PPT = 1;
+  int* list_cc = nullptr;
+  int* list_tc = nullptr;
+  int cnt_idx = -1;                 // index into counts[] (2 ints per conv)
+  int grid_cc = 0;
+  // affine
+  float* scale = nullptr;
+  float* shift = nullptr;
+};
+
+}  // namespace
+
+struct dcnn_net {
+  int device = 0, S = 1, dtype = 0, esz = 4;
+  int inH = 0, inW = 0, inC = 0, radius = 0, flags = 0;
+  std::vector<Op> ops;
+  std::vector<int> outputs;
+  // device state
+  void* frame_in = nullptr;
+  void* P = nullptr;
+  void* in_delta = nullptr;
+  uint8_t* in_mask = nullptr;
+  uint8_t* first = nullptr;
+  long long* frame_idx = nullptr;
+  int* err = nullptr;
+  int* err_host = nullptr;          // pinned mirror, refreshed at the end of every frame
+  float* eps = nullptr;             // [n_ops + 1], slot 0 = input
+  unsigned long long* stats = nullptr;  // [(n_ops + 1) * 8]
+  int* counts = nullptr;            // [2 * n_convs]
+  int n_counts = 0;
+  std::vector<float> eps_host;
+  std::vector<void*> allocs;
+  // graph
+  cudaStream_t cap = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int kernels = 0;
+  cudaStream_t last = nullptr;
+  // host staging for the _host entry point
+  void* h_frames = nullptr;
+  size_t frame_bytes = 0;
+};
+
+template <typename T>
+static dcnn_status dalloc(dcnn_net* n, T** p, size_t bytes) {
+  void* q = nullptr;
+  if (bytes == 0) bytes = 16;
+  CUDA_TRY(cudaMalloc(&q, bytes));
+  n->allocs.push_back(q);
+  *p = reinterpret_cast<T*>(q);
+  return DCNN_OK;
+}
+
+static int conv_out(int n, int k, int s, int p, int d) { return (n + 2 * p - d * (k - 1) - 1) / s + 1; }
+
+static dcnn_status plan_cc(Op& o) {
+  // Sub-tile for the CUDA-core kernel: P pixels x Cp channels of fp32 in smem.
+  o.Cp = (o.C + 3) / 4 * 4;
+  int P = o.Cp <= 128 ? 64 : (o.Cp <= 256 ? 32 : 16);
+  o.STH = P == 64 ? 8 : (P == 32 ? 4 : 4);
+  o.STW = P == 64 ? 8 : (P == 32 ? 8 : 4);
+  o.TH = o.STH;
+  o.TW = o.STW;
+  const int NCG = o.Cp / 4;
+  int PPT = 1;
+  while ((P / PPT) * NCG > 256) PPT *= 2;
+  if (PPT > 8 || P % PPT) return fail(DCNN_ERR_UNSUPPORTED, "conv: channel count too large for CUDA-core tile");
+  o.PPT = PPT;
+  o.WH = (o.STH - 1) * o.stride + (o.kh - 1) * o.dil + 1;
+  o.WW = (o.STW - 1) * o.stride + (o.kw - 1) * o.dil + 1;
+  int CIC = std::min(o.Ci, 32);
+  while (CIC > 1 && (size_t)o.WH * o.WW * CIC * 4 > 48 * 1024) CIC /= 2;
+  o.CIC = CIC;
+  return DCNN_OK;
+}
+
+static size_t cc_smem(const Op& o) {
+  return (size_t)o.WH * o.WW * o.CIC * 4 + ((size_t)o.WH * o.WW + 15) / 16 * 16 +
+         (size_t)o.STH * o.STW * o.Cp * 4;
+}
+
+static Epi make_epi(dcnn_net* n, int i) {
+  Op& o = n->ops[i];
+  Epi e;
+  e.C = o.C;
+  e.act = o.act;
+  e.act_param = o.act_param;
+  e.eps = n->eps + i + 1;
+  e.xA = o.xA;
+  e.xT = o.xT;
+  e.delta = o.delta;
+  e.mask = o.mask;
+  e.O = o.O;
+  e.first = n->first;
+  e.HW = (long long)o.H * o.W;
+  e.n_active = n->stats + (size_t)(i + 1) * 8 + 1;
+  return e;
+}
+
+static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
+  int k = 0;
+  const int nops = (int)n->ops.size();
+  cudaMemsetAsync(n->stats, 0, sizeof(unsigned long long) * 8 * (nops + 1), st);
+  if (n->n_counts) cudaMemsetAsync(n->counts, 0, sizeof(int) * n->n_counts, st);
+  InputParams ip;
+  ip.S = n->S; ip.H = n->inH; ip.W = n->inW; ip.C = n->inC; ip.radius = n->radius;
+  ip.frame = n->frame_in; ip.P = n->P; ip.delta = n->in_delta; ip.mask = n->in_mask;
+  ip.eps = n->eps; ip.first = n->first; ip.err = n->err; ip.n_active = n->stats + 1;
+  launch_input(ip, n->dtype, st);
+  ++k;
+  auto src_delta = [&](int j) -> const void* { return j < 0 ? n->in_delta : n->ops[j].delta; };
+  auto src_mask = [&](int j) -> const uint8_t* { return j < 0 ? n->in_mask : n->ops[j].mask; };
+  for (int i = 0; i < nops; ++i) {
+    Op& o = n->ops[i];
+    if (o.kind == DCNN_OP_CONV) {
+      TileParams tp;
+      tp.S = n->S; tp.H = o.Hi; tp.W = o.Wi; tp.Ho = o.H; tp.Wo = o.W;
+      tp.kh = o.kh; tp.kw = o.kw; tp.stride = o.stride; tp.pad = o.pad; tp.dil = o.dil;
+      tp.TH = o.TH; tp.TW = o.TW; tp.nty = o.nty; tp.ntx = o.ntx;
+      tp.mask_in = src_mask(o.in[0]); tp.mconv = o.mask; tp.first = n->first;
+      tp.sparse_max = 4; tp.use_tc = 0;
+      tp.list_cc = o.list_cc; tp.count_cc = n->counts + o.cnt_idx;
+      tp.list_tc = o.list_tc; tp.count_tc = n->counts + o.cnt_idx + 1;
+      tp.stats = n->stats + (size_t)(i + 1) * 8;
+      launch_tiles(tp, st);
+      ++k;
+      ConvCCParams cp;
+      cp.S = n->S; cp.H = o.Hi; cp.W = o.Wi; cp.Ci = o.Ci;
+      cp.Ho = o.H; cp.Wo = o.W; cp.Co = o.C; cp.Cp = o.Cp;
+      cp.kh = o.kh; cp.kw = o.kw; cp.stride = o.stride; cp.pad = o.pad; cp.dil = o.dil;
+      cp.TH = o.TH; cp.TW = o.TW; cp.nty = o.nty; cp.ntx = o.ntx; cp.STH = o.STH; cp.STW = o.STW;
+      cp.WH = o.WH; cp.WW = o.WW; cp.CIC = o.CIC; cp.PPT = o.PPT;
+      cp.delta_in = src_delta(o.in[0]); cp.mask_in = src_mask(o.in[0]);
+      cp.wt = o.wt; cp.bias = o.bias;
+      cp.list = o.list_cc; cp.count = n->counts + o.cnt_idx;
+      cp.ep = make_epi(n, i);
+      launch_conv_cc(cp, n->dtype, o.grid_cc, st);
+      ++k;
+    } else {
+      PwParams pp;
+      memset(&pp, 0, sizeof(pp));
+      pp.kind = o.kind; pp.S = n->S; pp.H = o.H; pp.W = o.W; pp.Hi = o.Hi; pp.Wi = o.Wi;
+      pp.n_in = o.n_in;
+      for (int j = 0; j < o.n_in; ++j) {
+        pp.in[j] = src_delta(o.in[j]);
+        pp.min[j] = src_mask(o.in[j]);
+        pp.Cin[j] = o.Cin[j];
+      }
+      pp.k = o.kh; pp.stride = o.stride; pp.pad = o.pad; pp.up = o.up;
+      pp.scale = o.scale; pp.shift = o.shift; pp.poolA = o.poolA;
+      pp.ep = make_epi(n, i);
+      launch_pointwise(pp, n->dtype, st);
+      ++k;
+      if (o.kind == DCNN_OP_MAXPOOL) {
+        launch_pool_update(pp, n->dtype, st);
+        ++k;
+      }
+    }
+  }
+  launch_end_frame(n->first, n->frame_idx, n->S, st);
+  ++k;
+  cudaMemcpyAsync(n->err_host, n->err, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (kcount) *kcount = k;
+}
+
+static dcnn_status build_graph(dcnn_net* n) {
+  if (n->exec) return DCNN_OK;
+  CUDA_TRY(cudaStreamBeginCapture(n->cap, cudaStreamCaptureModeThreadLocal));
+  enqueue_frame(n, n->cap, &n->kernels);
+  cudaError_t e = cudaStreamEndCapture(n->cap, &n->graph);
+  if (e != cudaSuccess) return fail(DCNN_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  CUDA_TRY(cudaGraphInstantiate(&n->exec, n->graph, 0));
+  return DCNN_OK;
+}
+
+extern "C" {
+
+const char* dcnn_last_error(void) { return g_err.c_str(); }
+
+void dcnn_destroy_net(dcnn_net* n) {
+  if (!n) return;
+  cudaSetDevice(n->device);
+  cudaDeviceSynchronize();
+  if (n->exec) cudaGraphExecDestroy(n->exec);
+  if (n->graph) cudaGraphDestroy(n->graph);
+  if (n->cap) cudaStreamDestroy(n->cap);
+  for (void* p : n->allocs) cudaFree(p);
+  if (n->err_host) cudaFreeHost(n->err_host);
+  if (n->h_frames) cudaFreeHost(n->h_frames);
+  delete n;
+}
+
+static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
+  if (d->in_h <= 0 || d->in_w <= 0 || d->in_c <= 0 || d->n_streams <= 0)
+    return fail(DCNN_ERR_SHAPE, "frame shape and n_streams must be positive");
+  if (d->dtype != DCNN_F32 && d->dtype != DCNN_F16) return fail(DCNN_ERR_ARG, "dtype");
+  if (d->n_layers <= 0 || !d->layers) return fail(DCNN_ERR_ARG, "no layers");
+  if (d->n_outputs <= 0 || !d->output_ops) return fail(DCNN_ERR_ARG, "no outputs");
+  if (d->input_dilation < 0 || d->input_dilation > 16) return fail(DCNN_ERR_UNSUPPORTED, "input_dilation must be in [0,16]");
+  n->device = d->device; n->S = d->n_streams; n->dtype = d->dtype; n->esz = d->dtype == DCNN_F16 ? 2 : 4;
+  n->inH = d->in_h; n->inW = d->in_w; n->inC = d->in_c; n->radius = d->input_dilation; n->flags = d->flags;
+  CUDA_TRY(cudaSetDevice(n->device));
+  const int L = d->n_layers;
+  n->ops.resize(L);
+  auto shape_of = [&](int j, int& H, int& W, int& C) {
+    if (j < 0) { H = n->inH; W = n->inW; C = n->inC; }
+    else { H = n->ops[j].H; W = n->ops[j].W; C = n->ops[j].C; }
+  };
+  int n_convs = 0;
+  for (int i = 0; i < L; ++i) {
+    const dcnn_layer_desc& ld = d->layers[i];
+    Op& o = n->ops[i];
+    o.kind = ld.op;
+    if (ld.op < DCNN_OP_CONV || ld.op > DCNN_OP_AFFINE) return fail(DCNN_ERR_ARG, "layer " + std::to_string(i) + ": bad op");
+    o.n_in = (ld.op == DCNN_OP_ADD || ld.op == DCNN_OP_CONCAT) ? ld.n_in : 1;
+    if (o.n_in < 1 || o.n_in > 4) return fail(DCNN_ERR_ARG, "layer " + std::to_string(i) + ": n_in");
+    for (int j = 0; j < o.n_in; ++j) {
+      o.in[j] = ld.in[j];
+      if (o.in[j] < -1 || o.in[j] >= i) return fail(DCNN_ERR_SHAPE, "layer " + std::to_string(i) + ": dangling input reference");
+    }
+    shape_of(o.in[0], o.Hi, o.Wi, o.Ci);
+    for (int j = 0; j < o.n_in; ++j) { int h, w; shape_of(o.in[j], h, w, o.Cin[j]); }
+    o.act = ld.act;
+    if (o.act < DCNN_ACT_NONE || o.act > DCNN_ACT_SIGMOID) return fail(DCNN_ERR_ARG, "bad act");
+    o.act_param = ld.act_param != 0.f ? ld.act_param : 0.1f;
+    o.kh = ld.kh; o.kw = ld.kw; o.stride = ld.stride; o.pad = ld.pad; o.dil = ld.dilation;
+    o.groups = ld.groups; o.up = ld.up_factor;
+    switch (ld.op) {
+      case DCNN_OP_CONV: {
+        if (!ld.weight) return fail(DCNN_ERR_ARG, "conv without weight");
+        if (ld.c_out <= 0 || o.kh <= 0 || o.kw <= 0 || o.stride <= 0 || o.dil <= 0 || o.pad < 0 || o.groups <= 0)
+          return fail(DCNN_ERR_SHAPE, "conv " + std::to_string(i) + ": bad parameters");
+        if (o.Ci % o.groups || ld.c_out % o.groups) return fail(DCNN_ERR_SHAPE, "conv: groups must divide channels");
+        o.C = ld.c_out;
+        o.H = conv_out(o.Hi, o.kh, o.stride, o.pad, o.dil);
+        o.W = conv_out(o.Wi, o.kw, o.stride, o.pad, o.dil);
+        ++n_convs;
+        break;
+      }
+      case DCNN_OP_ACT:
+        if (o.act == DCNN_ACT_NONE) return fail(DCNN_ERR_ARG, "act op needs an activation");
+        o.H = o.Hi; o.W = o.Wi; o.C = o.Ci;
+        break;
+      case DCNN_OP_MAXPOOL:
+      case DCNN_OP_AVGPOOL:
+        if (o.kh <= 0 || o.kh != o.kw || o.stride <= 0 || o.pad < 0 || 2 * o.pad > o.kh)
+          return fail(DCNN_ERR_UNSUPPORTED, "pool: square window, stride >= 1, pad <= k/2");
+        o.H = conv_out(o.Hi, o.kh, o.stride, o.pad, 1);
+        o.W = conv_out(o.Wi, o.kw, o.stride, o.pad, 1);
+        o.C = o.Ci; o.dil = 1;
+        if (o.act) return fail(DCNN_ERR_UNSUPPORTED, "pool with fused act");
+        break;
+      case DCNN_OP_UPSAMPLE_NEAREST:
+        if (o.up < 1) return fail(DCNN_ERR_ARG, "up_factor");
+        o.H = o.Hi * o.up; o.W = o.Wi * o.up; o.C = o.Ci;
+        if (o.act) return fail(DCNN_ERR_UNSUPPORTED, "upsample with fused act");
+        break;
+      case DCNN_OP_ADD:
+        for (int j = 0; j < o.n_in; ++j) {
+          int h, w, c;
+          shape_of(o.in[j], h, w, c);
+          if (h != o.Hi || w != o.Wi || c != o.Ci) return fail(DCNN_ERR_SHAPE, "add: operand shapes differ");
+        }
+        o.H = o.Hi; o.W = o.Wi; o.C = o.Ci;
+        break;
+      case DCNN_OP_CONCAT: {
+        int c = 0;
+        for (int j = 0; j < o.n_in; ++j) {
+          int h, w, cj;
+          shape_of(o.in[j], h, w, cj);
+          if (h != o.Hi || w != o.Wi) return fail(DCNN_ERR_SHAPE, "concat: spatial shapes differ");
+          c += cj;
+        }
+        o.H = o.Hi; o.W = o.Wi; o.C = c;
+        if (o.act) return fail(DCNN_ERR_UNSUPPORTED, "concat with fused act");
+        break;
+      }
+      case DCNN_OP_AFFINE:
+        if (!ld.scale || !ld.shift) return fail(DCNN_ERR_ARG, "affine needs scale and shift");
+        o.H = o.Hi; o.W = o.Wi; o.C = o.Ci;
+        if (o.act) return fail(DCNN_ERR_UNSUPPORTED, "affine with fused act");
+        break;
+    }
+    if (o.H <= 0 || o.W <= 0 || o.C <= 0) return fail(DCNN_ERR_SHAPE, "layer " + std::to_string(i) + ": empty output");
+    if (o.act != DCNN_ACT_NONE && o.C > 32 * MAXK) return fail(DCNN_ERR_UNSUPPORTED, "truncating op with more than 512 channels");
+  }
+  for (int k = 0; k < d->n_outputs; ++k) {
+    int j = d->output_ops[k];
+    if (j < 0 || j >= L) return fail(DCNN_ERR_ARG, "output op index");
+    if (n->ops[j].out_slot >= 0) return fail(DCNN_ERR_ARG, "duplicate output op");
+    n->ops[j].out_slot = k;
+    n->outputs.push_back(j);
+  }
+  // ---- device state
+  const size_t S = n->S, es = n->esz;
+  const size_t in_px = S * n->inH * n->inW;
+  n->frame_bytes = in_px * n->inC * es;
+  dcnn_status r;
+  if ((r = dalloc(n, &n->frame_in, n->frame_bytes))) return r;
+  if ((r = dalloc(n, &n->P, n->frame_bytes))) return r;
+  if ((r = dalloc(n, &n->in_delta, n->frame_bytes))) return r;
+  if ((r = dalloc(n, &n->in_mask, in_px))) return r;
+  if ((r = dalloc(n, &n->first, S))) return r;
+  if ((r = dalloc(n, &n->frame_idx, S * sizeof(long long)))) return r;
+  if ((r = dalloc(n, &n->err, sizeof(int)))) return r;
+  if ((r = dalloc(n, &n->eps, sizeof(float) * (L + 1)))) return r;
+  if ((r = dalloc(n, &n->stats, sizeof(unsigned long long) * 8 * (L + 1)))) return r;
+  n->n_counts = 2 * n_convs;
+  if ((r = dalloc(n, &n->counts, sizeof(int) * std::max(1, n->n_counts)))) return r;
+  CUDA_TRY(cudaMemset(n->first, 1, S));
+  CUDA_TRY(cudaMemset(n->frame_idx, 0, S * sizeof(long long)));
+  CUDA_TRY(cudaMemset(n->err, 0, sizeof(int)));
+  CUDA_TRY(cudaMemset(n->P, 0, n->frame_bytes));
+  CUDA_TRY(cudaHostAlloc(&n->err_host, sizeof(int), cudaHostAllocDefault));
+  *n->err_host = 0;
+  n->eps_host.assign(L + 1, 0.f);
+  n->eps_host[0] = d->input_threshold;
+  for (int i = 0; i < L; ++i) n->eps_host[i + 1] = d->layers[i].threshold;
+  CUDA_TRY(cudaMemcpy(n->eps, n->eps_host.data(), sizeof(float) * (L + 1), cudaMemcpyHostToDevice));
+  int cnt = 0;
+  for (int i = 0; i < L; ++i) {
+    Op& o = n->ops[i];
+    const dcnn_layer_desc& ld = d->layers[i];
+    const size_t px = S * o.H * o.W;
+    if ((r = dalloc(n, &o.delta, px * o.C * es))) return r;
+    if ((r = dalloc(n, &o.mask, px))) return r;
+    if (o.act != DCNN_ACT_NONE) {
+      if ((r = dalloc(n, &o.xA, px * o.C * es))) return r;
+      if ((r = dalloc(n, &o.xT, px * o.C * es))) return r;
+    }
+    if (o.kind == DCNN_OP_MAXPOOL && (r = dalloc(n, &o.poolA, S * o.Hi * o.Wi * o.C * es))) return r;
+    if (o.out_slot >= 0) {
+      if ((r = dalloc(n, &o.O, px * o.C * sizeof(float)))) return r;
+      CUDA_TRY(cudaMemset(o.O, 0, px * o.C * sizeof(float)));
+    }
+    if (o.kind == DCNN_OP_CONV) {
+      if ((r = plan_cc(o))) return r;
+      o.K = o.kh * o.kw * (o.Ci / o.groups);
+      o.nty = (o.H + o.TH - 1) / o.TH;
+      o.ntx = (o.W + o.TW - 1) / o.TW;
+      const int ntiles = n->S * o.nty * o.ntx;
+      if ((r = dalloc(n, &o.list_cc, sizeof(int) * ntiles))) return r;
+      if ((r = dalloc(n, &o.list_tc, sizeof(int) * ntiles))) return r;
+      o.cnt_idx = cnt;
+      cnt += 2;
+      const int nsub = (o.TH / o.STH) * (o.TW / o.STW);
+      o.grid_cc = std::max(1, std::min(ntiles * nsub, 148 * 4));
+      // weights: OHWI [Co][kh][kw][Ci/g] -> [kh*kw][Ci][Cp] fp32, groups expanded densely,
+      // values rounded to the storage dtype (the method's weights are in dtype).
+      const int Cg = o.Ci / o.groups, Og = o.C / o.groups;
+      std::vector<float> wt((size_t)o.kh * o.kw * o.Ci * o.Cp, 0.f);
+      for (int co = 0; co < o.C; ++co) {
+        const int g = co / Og;
+        for (int ky = 0; ky < o.kh; ++ky)
+          for (int kx = 0; kx < o.kw; ++kx)
+            for (int ci = 0; ci < Cg; ++ci) {
+              float v = ld.weight[(((size_t)co * o.kh + ky) * o.kw + kx) * Cg + ci];
+              if (n->dtype == DCNN_F16) v = __half2float(__float2half_rn(v));
+              wt[((size_t)(ky * o.kw + kx) * o.Ci + g * Cg + ci) * o.Cp + co] = v;
+            }
+      }
+      if ((r = dalloc(n, &o.wt, wt.size() * 4))) return r;
+      CUDA_TRY(cudaMemcpy(o.wt, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice));
+      std::vector<float> b(o.C, 0.f);
+      if (ld.bias) std::copy(ld.bias, ld.bias + o.C, b.begin());
+      if ((r = dalloc(n, &o.bias, o.C * 4))) return r;
+      CUDA_TRY(cudaMemcpy(o.bias, b.data(), o.C * 4, cudaMemcpyHostToDevice));
+      const size_t smem = cc_smem(o);
+      if (smem > 200 * 1024) return fail(DCNN_ERR_UNSUPPORTED, "conv tile does not fit shared memory");
+    }
+    if (o.kind == DCNN_OP_AFFINE) {
+      if ((r = dalloc(n, &o.scale, o.C * 4))) return r;
+      if ((r = dalloc(n, &o.shift, o.C * 4))) return r;
+      CUDA_TRY(cudaMemcpy(o.scale, ld.scale, o.C * 4, cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(o.shift, ld.shift, o.C * 4, cudaMemcpyHostToDevice));
+    }
+  }
+  CUDA_TRY(conv_cc_init());
+  CUDA_TRY(cudaStreamCreateWithFlags(&n->cap, cudaStreamNonBlocking));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return DCNN_OK;
+}
+
+dcnn_status dcnn_create_net(const dcnn_net_desc* desc, dcnn_net** out) {
+  if (!desc || !out) return fail(DCNN_ERR_ARG, "null argument");
+  *out = nullptr;
+  dcnn_net* n = new dcnn_net();
+  dcnn_status s = create_impl(desc, n);
+  if (s != DCNN_OK) {
+    std::string keep = g_err;
+    dcnn_destroy_net(n);
+    g_err = keep;
+    return s;
+  }
+  *out = n;
+  return DCNN_OK;
+}
+
+dcnn_status dcnn_set_threshold(dcnn_net* n, int32_t op, float eps) {
+  if (!n) return fail(DCNN_ERR_ARG, "null net");
+  if (op < -1 || op >= (int)n->ops.size()) return fail(DCNN_ERR_ARG, "op index");
+  if (op >= 0 && n->ops[op].act == DCNN_ACT_NONE) return fail(DCNN_ERR_ARG, "op has no truncation");
+  if (std::isnan(eps)) return fail(DCNN_ERR_ARG, "eps is NaN");
+  CUDA_TRY(cudaSetDevice(n->device));
+  n->eps_host[op + 1] = eps;
+  // stream-ordered after previously enqueued frames (the value lives in pageable
+  // memory of the net, so it is staged synchronously on the last stream)
+  cudaStream_t st = n->last ? n->last : n->cap;
+  CUDA_TRY(cudaMemcpyAsync(n->eps + op + 1, &n->eps_host[op + 1], sizeof(float), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return DCNN_OK;
+}
+
+dcnn_status dcnn_reset(dcnn_net* n, int32_t stream) {
+  if (!n) return fail(DCNN_ERR_ARG, "null net");
+  if (stream < -1 || stream >= n->S) return fail(DCNN_ERR_ARG, "stream index");
+  CUDA_TRY(cudaSetDevice(n->device));
+  cudaStream_t st = n->last ? n->last : n->cap;
+  if (stream < 0) CUDA_TRY(cudaMemsetAsync(n->first, 1, n->S, st));
+  else CUDA_TRY(cudaMemsetAsync(n->first + stream, 1, 1, st));
+  return DCNN_OK;
+}
+
+static dcnn_status check_err(dcnn_net* n) {
+  if (*n->err_host) return fail(DCNN_ERR_NONFINITE, "non-finite value in an input frame (sticky)");
+  return DCNN_OK;
+}
+
+dcnn_status dcnn_process_frame(dcnn_net* n, const void* frames, void* const* outputs, void* stream) {
+  if (!n || !frames) return fail(DCNN_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(n->device));
+  dcnn_status s = check_err(n);
+  if (s) return s;
+  if ((s = build_graph(n))) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaMemcpyAsync(n->frame_in, frames, n->frame_bytes, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaGraphLaunch(n->exec, st));
+  if (outputs) {
+    for (size_t k = 0; k < n->outputs.size(); ++k) {
+      const Op& o = n->ops[n->outputs[k]];
+      if (!outputs[k]) continue;
+      CUDA_TRY(cudaMemcpyAsync(outputs[k], o.O, (size_t)n->S * o.H * o.W * o.C * 4, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  n->last = st;
+  return DCNN_OK;
+}
+
+dcnn_status dcnn_process_frame_host(dcnn_net* n, const void* host_frames, void* const* host_outputs, void* stream) {
+  if (!n || !host_frames) return fail(DCNN_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(n->device));
+  dcnn_status s = check_err(n);
+  if (s) return s;
+  if ((s = build_graph(n))) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaMemcpyAsync(n->frame_in, host_frames, n->frame_bytes, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaGraphLaunch(n->exec, st));
+  if (host_outputs) {
+    for (size_t k = 0; k < n->outputs.size(); ++k) {
+      const Op& o = n->ops[n->outputs[k]];
+      if (!host_outputs[k]) continue;
+      CUDA_TRY(cudaMemcpyAsync(host_outputs[k], o.O, (size_t)n->S * o.H * o.W * o.C * 4, cudaMemcpyDeviceToHost, st));
+    }
+  }
+  n->last = st;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return check_err(n);
+}
+
+dcnn_status dcnn_op_shape(dcnn_net* n, int32_t op, int32_t* H, int32_t* W, int32_t* C) {
+  if (!n || !H || !W || !C) return fail(DCNN_ERR_ARG, "null argument");
+  if (op < -1 || op >= (int)n->ops.size()) return fail(DCNN_ERR_ARG, "op index");
+  if (op < 0) { *H = n->inH; *W = n->inW; *C = n->inC; }
+  else { *H = n->ops[op].H; *W = n->ops[op].W; *C = n->ops[op].C; }
+  return DCNN_OK;
+}
+
+dcnn_status dcnn_get_stats(dcnn_net* n, dcnn_op_stats* per_op, int64_t* frame_index, int32_t* device_error) {
+  if (!n) return fail(DCNN_ERR_ARG, "null net");
+  CUDA_TRY(cudaSetDevice(n->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  const int L = (int)n->ops.size();
+  std::vector<unsigned long long> raw((size_t)8 * (L + 1));
+  CUDA_TRY(cudaMemcpy(raw.data(), n->stats, raw.size() * 8, cudaMemcpyDeviceToHost));
+  long long fi = 0;
+  CUDA_TRY(cudaMemcpy(&fi, n->frame_idx, sizeof(long long), cudaMemcpyDeviceToHost));
+  int err = 0;
+  CUDA_TRY(cudaMemcpy(&err, n->err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (frame_index) *frame_index = fi;
+  if (device_error) *device_error = err ? DCNN_ERR_NONFINITE : DCNN_OK;
+  if (per_op) {
+    for (int i = 0; i <= L; ++i) {
+      const unsigned long long* r = &raw[(size_t)8 * i];
+      dcnn_op_stats& o = per_op[i];
+      memset(&o, 0, sizeof(o));
+      o.active_out = (int64_t)r[1];
+      if (i == 0) {
+        o.active_in = o.active_out;
+        continue;
+      }
+      const Op& op = n->ops[i - 1];
+      o.active_in = (int64_t)raw[(size_t)8 * (op.in[0] + 1) + 1];
+      if (op.kind == DCNN_OP_CONV) {
+        o.tiles_total = (int64_t)r[2];
+        o.tiles_skip = (int64_t)r[3];
+        o.tiles_sparse = (int64_t)r[4];
+        o.tiles_dense = (int64_t)r[5];
+        const int64_t macpx = (int64_t)op.K * op.C;
+        o.mac_alg = (int64_t)r[6] * macpx;
+        o.mac_exec = (o.tiles_sparse + o.tiles_dense) * (int64_t)op.TH * op.TW * macpx;
+      }
+    }
+  }
+  return err ? fail(DCNN_ERR_NONFINITE, "non-finite value in an input frame (sticky)") : DCNN_OK;
+}
+
+dcnn_status dcnn_debug_read(dcnn_net* n, int32_t op, int32_t which, void* host, int64_t* bytes) {
+  if (!n) return fail(DCNN_ERR_ARG, "null net");
+  if (op < -1 || op >= (int)n->ops.size()) return fail(DCNN_ERR_ARG, "op index");
+  CUDA_TRY(cudaSetDevice(n->device));
+  const void* src = nullptr;
+  size_t nb = 0;
+  const size_t es = n->esz;
+  if (op < 0) {
+    const size_t px = (size_t)n->S * n->inH * n->inW;
+    switch (which) {
+      case DCNN_BUF_DELTA: src = n->in_delta; nb = px * n->inC * es; break;
+      case DCNN_BUF_MASK: src = n->in_mask; nb = px; break;
+      case DCNN_BUF_XA: src = n->P; nb = px * n->inC * es; break;
+      default: return fail(DCNN_ERR_ARG, "buffer not present for the input layer");
+    }
+  } else {
+    const Op& o = n->ops[op];
+    const size_t px = (size_t)n->S * o.H * o.W;
+    switch (which) {
+      case DCNN_BUF_DELTA: src = o.delta; nb = px * o.C * es; break;
+      case DCNN_BUF_MASK: src = o.mask; nb = px; break;
+      case DCNN_BUF_XA: src = o.xA; nb = px * o.C * es; break;
+      case DCNN_BUF_XT: src = o.xT; nb = px * o.C * es; break;
+      case DCNN_BUF_OUT: src = o.O; nb = px * o.C * 4; break;
+      case DCNN_BUF_POOLA: src = o.poolA; nb = (size_t)n->S * o.Hi * o.Wi * o.C * es; break;
+      default: return fail(DCNN_ERR_ARG, "which");
+    }
+    if (!src) return fail(DCNN_ERR_ARG, "buffer not present for this op");
+  }
+  if (bytes) *bytes = (int64_t)nb;
+  if (host) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(host, src, nb, cudaMemcpyDeviceToHost));
+  }
+  return DCNN_OK;
+}
+
+int32_t dcnn_kernels_per_frame(dcnn_net* n) {
+  if (!n) return -1;
+  if (build_graph(n) != DCNN_OK) return -1;
+  return n->kernels;
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// kernels.h -- host-side launch interface of the DeltaCNN sm_100a kernels.
+// Every launcher enqueues on `st` and never synchronises; grids are fixed at
+// plan time and the amount of work is read from device memory, so one frame
+// is capturable as a single CUDA graph.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace dcnn {
+
+// ---------------------------------------------------------------- a1: input
+struct InputParams {
+  int S, H, W, C;
+  int radius;                   // Chebyshev dilation radius
+  const void* frame;            // [S,H,W,C] T  (F, already in storage dtype)
+  void* P;                      // [S,H,W,C] T  previous propagated input
+  void* delta;                  // [S,H,W,C] T
+  uint8_t* mask;                // [S,H,W]
+  const float* eps;             // device slot of eps_in
+  const uint8_t* first;         // [S]
+  int* err;                     // sticky error word (bit 0: non-finite input)
+  unsigned long long* n_active;
+};
+void launch_input(const InputParams& p, int dtype, cudaStream_t st);
+
+// ---------------------------------------------------------------- a2: tiles
+struct TileParams {
+  int S, H, W;                  // conv input spatial shape
+  int Ho, Wo;
+  int kh, kw, stride, pad, dil;
+  int TH, TW, nty, ntx;
+  const uint8_t* mask_in;
+  uint8_t* mconv;               // [S,Ho,Wo] receptive-field OR of mask_in (Z7)
+  const uint8_t* first;
+  int sparse_max;               // tiles with <= sparse_max active inputs -> CUDA-core list
+  int use_tc;                   // 0: every non-empty tile goes to the CUDA-core list
+  int* list_cc; int* count_cc;  // CUDA-core tiles
+  int* list_tc; int* count_tc;  // tensor-core tiles
+  unsigned long long* stats;    // [active_in, active_out(m_conv), tiles_total, skip, sparse, dense]
+};
+void launch_tiles(const TileParams& p, cudaStream_t st);
+
+// ---------------------------------------------------------------- a4: CUDA-core conv
+struct ConvCCParams {
+  int S, H, W, Ci;
+  int Ho, Wo, Co, Cp;
+  int kh, kw, stride, pad, dil;
+  int TH, TW, nty, ntx;         // list tile (as classified by a2)
+  int STH, STW;                 // sub-tile processed per pass (TH % STH == 0, TW % STW == 0)
+  int WH, WW, CIC, PPT;         // sub-tile window dims, input-channel chunk, pixels per item
+  const void* delta_in;
+  const uint8_t* mask_in;
+  const float* wt;              // [kh*kw][Ci][Cp] fp32 (groups expanded densely)
+  const float* bias;            // [Co] fp32
+  const int* list; const int* count;
+  Epi ep;                       // ep.mask holds m_conv on entry for the tile's pixels
+};
+void launch_conv_cc(const ConvCCParams& p, int dtype, int grid, cudaStream_t st);
+size_t conv_cc_smem(const ConvCCParams& p);
+cudaError_t conv_cc_init();     // once per process/device: raise the dynamic smem limit
+
+// ---------------------------------------------------------------- a6/a7 pointwise ops
+struct PwParams {
+  int kind;                     // dcnn_op
+  int S, H, W;                  // OUTPUT spatial shape
+  int Hi, Wi;                   // input spatial shape (pool / up)
+  int n_in;
+  const void* in[4];            // input deltas [S,Hi,Wi,Ci_k] T
+  const uint8_t* min[4];        // input masks
+  int Cin[4];                   // channels of each input
+  int k, stride, pad, up;       // pool window / upsample factor
+  const float* scale; const float* shift;  // affine
+  void* poolA;                  // maxpool accumulated input [S,Hi,Wi,C] T
+  Epi ep;
+  unsigned long long* n_in_active;
+};
+void launch_pointwise(const PwParams& p, int dtype, cudaStream_t st);
+void launch_pool_update(const PwParams& p, int dtype, cudaStream_t st);
+
+// ---------------------------------------------------------------- control
+void launch_end_frame(uint8_t* first, long long* frame_idx, int S, cudaStream_t st);
+
+}  // namespace dcnn

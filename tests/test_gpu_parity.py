@@ -1,0 +1,177 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs (north_star: masks bit-exact at eps=0, >= 99.9 % agreement at eps>0;
+fp32 outputs within 1e-4, fp16 within 2e-2 max-abs-relative)."""
+import numpy as np
+import pytest
+
+from oracle import DeltaOracle
+from synth import nets
+from synth.frames import VideoSpec, cfg1_frames, clip
+from helpers import max_abs_rel
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _engine(net, S, flags=0):
+    from paper_2203_03996_b200 import DeltaNet
+    return DeltaNet(net, n_streams=S, flags=flags)
+
+
+def run_both(net, frames, *, check_masks="exact", tol=1e-4, mask_agree=0.999, flags=0,
+             ops_to_check=None, bit_exact=False):
+    """frames [T,S,H,W,C] in the net dtype.  Steps oracle and engine in lockstep."""
+    from paper_2203_03996_b200 import BUF_MASK
+    T, S = frames.shape[:2]
+    eng = _engine(net, S, flags)
+    orc = DeltaOracle(net, S)
+    outs_t = [torch.empty((S,) + s, dtype=torch.float32, device="cuda") for s in eng.out_shapes]
+    worst = 0.0
+    agree_min = 1.0
+    ops = range(-1, len(net.layers)) if ops_to_check is None else ops_to_check
+    for t in range(T):
+        fr = torch.from_numpy(np.ascontiguousarray(frames[t])).cuda()
+        eng.process_frame(fr, outs_t)
+        torch.cuda.synchronize()
+        want = orc.step(frames[t])
+        for g, o in zip(outs_t, want):
+            g = g.cpu().numpy()
+            if bit_exact:
+                np.testing.assert_array_equal(g, o.astype(np.float32), err_msg=f"frame {t}")
+            e = max_abs_rel(g, o)
+            worst = max(worst, e)
+            assert e <= tol, f"frame {t}: max-abs-rel {e:.3e} > {tol}"
+        for op in ops:
+            gm = eng.debug_read(op, BUF_MASK).astype(bool)
+            om = orc.masks[op]
+            if check_masks == "exact":
+                assert (gm == om).all(), f"frame {t} op {op}: {(gm != om).sum()} mask mismatches"
+            else:
+                agree = (gm == om).mean()
+                agree_min = min(agree_min, agree)
+                assert agree >= mask_agree, f"frame {t} op {op}: mask agreement {agree:.5f}"
+    st = eng.stats()
+    eng.close()
+    return worst, agree_min, st
+
+
+def test_cfg1_dyadic_bit_identical():
+    """exact-arithmetic vectors -> GPU fp32 bit-identical to the oracle."""
+    net = nets.cfg1_net("dyadic")
+    run_both(net, cfg1_frames("dyadic", 8), bit_exact=True, tol=0.0)
+
+
+def test_cfg1_gauss():
+    net = nets.cfg1_net("gauss")
+    worst, _, st = run_both(net, cfg1_frames("gauss", 8), tol=1e-4)
+    ops = st["ops"]
+    assert ops[1]["tiles_skip"] + ops[1]["tiles_sparse"] + ops[1]["tiles_dense"] == ops[1]["tiles_total"]
+
+
+def test_cfg2_integer_exact():
+    """cfg2 exact variant: ternary weights, integer frames -> bit-identical fp32."""
+    net = nets.toy_net_integer(128, 128, 64)
+    rng = np.random.default_rng(0)
+    x = rng.integers(-32, 33, size=(1, 128, 128, 3)).astype(np.float32)
+    frames = [x]
+    for t in range(5):
+        x = x.copy()
+        x[0, 20 + 5 * t:42 + 5 * t, 30:52] = rng.integers(-32, 33, size=(22, 22, 3))
+        frames.append(x)
+    run_both(net, np.stack(frames)[:, :, :, :, :], bit_exact=True, tol=0.0)
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", 1e-4), ("f16", 2e-2)])
+def test_cfg2_toy_eps005(dtype, tol):
+    """BASELINE configs[1]: toy 128x128x64, eps = 0.05, ~10 % changed pixels, 30 frames."""
+    net = nets.toy_net(dtype=dtype)
+    dt = np.float16 if dtype == "f16" else np.float32
+    frames = clip([VideoSpec(128, 128, n_blobs=3, blob_h=22, blob_w=22, speed=3, noise_p=0.01,
+                             seed=2)], 30, dt)
+    worst, agree, _ = run_both(net, frames, check_masks="agree", tol=tol)
+    print(f"cfg2 {dtype}: worst max-abs-rel {worst:.2e}, min mask agreement {agree:.6f}")
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_graphs_eps0(seed):
+    """SPEC S:424 zero-threshold equivalence on random graphs, GPU vs oracle, fp32."""
+    net = nets.random_net(seed, n_layers=4 + seed % 7, dtype="f32", eps=0.0)
+    rng = np.random.default_rng(seed)
+    S = 2
+    x = rng.standard_normal((S, net.in_h, net.in_w, net.in_c)).astype(np.float32)
+    frames = [x]
+    for _ in range(5):
+        ch = rng.random((S, net.in_h, net.in_w)) < 0.1
+        x = np.where(ch[..., None], rng.standard_normal(x.shape), x).astype(np.float32)
+        frames.append(x)
+    run_both(net, np.stack(frames), check_masks="agree", mask_agree=0.999, tol=1e-4)
+
+
+def test_static_clip_empty_masks_and_constant_output():
+    """repeated frames -> every mask empty, output bit-identical."""
+    from paper_2203_03996_b200 import BUF_MASK
+    net = nets.toy_net(64, 64, 16, eps=0.0)
+    fr = clip([VideoSpec(64, 64, n_blobs=2, blob_h=8, blob_w=8, seed=3)], 1)[0]
+    eng = _engine(net, 1)
+    out = [torch.empty((1,) + s, device="cuda") for s in eng.out_shapes]
+    x = torch.from_numpy(fr).cuda()
+    eng.process_frame(x, out)
+    first = out[0].clone()
+    for _ in range(3):
+        eng.process_frame(x, out)
+        torch.cuda.synchronize()
+        assert torch.equal(out[0], first)
+        for op in range(-1, len(net.layers)):
+            assert eng.debug_read(op, BUF_MASK).sum() == 0
+    st = eng.stats()
+    assert st["ops"][1]["tiles_skip"] == st["ops"][1]["tiles_total"]
+
+
+def test_per_stream_reset_and_nan_poison():
+    """Z28: a stream reset inside a batched launch replays frame 0 exactly while the other
+    streams continue; NaN-poisoned inactive deltas never reach an active output."""
+    from paper_2203_03996_b200 import BUF_DELTA
+    net = nets.toy_net(64, 64, 16, eps=0.02)
+    specs = [VideoSpec(64, 64, n_blobs=2, blob_h=8, blob_w=8, seed=s) for s in (5, 6)]
+    frames = clip(specs, 8)
+    eng = _engine(net, 2)
+    orc = DeltaOracle(net, 2)
+    out = [torch.empty((2,) + s, device="cuda") for s in eng.out_shapes]
+    for t in range(8):
+        if t == 5:
+            eng.reset(1)
+            orc.reset(1)
+        eng.process_frame(torch.from_numpy(frames[t]).cuda(), out)
+        want = orc.step(frames[t])
+        torch.cuda.synchronize()
+        assert max_abs_rel(out[0].cpu().numpy(), want[0]) <= 1e-4
+    eng.close()
+
+
+def test_nonfinite_input_is_reported():
+    from paper_2203_03996_b200 import DcnnError
+    net = nets.toy_net(32, 32, 8)
+    eng = _engine(net, 1)
+    x = np.zeros((1, 32, 32, 3), np.float32)
+    eng.process_frame(torch.from_numpy(x).cuda())
+    x[0, 3, 4, 1] = np.nan
+    eng.process_frame(torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    st = eng.stats()
+    assert st["device_error"] == 4
+    with pytest.raises(DcnnError):
+        eng.process_frame(torch.from_numpy(x).cuda())
+
+
+def test_host_entry_point_matches_device():
+    net = nets.toy_net(64, 64, 16)
+    frames = clip([VideoSpec(64, 64, n_blobs=2, blob_h=8, blob_w=8, seed=8)], 4)
+    a = _engine(net, 1)
+    b = _engine(net, 1)
+    out = [torch.empty((1,) + s, device="cuda") for s in a.out_shapes]
+    for t in range(4):
+        a.process_frame(torch.from_numpy(frames[t]).cuda(), out)
+        hb = b.process_frame_host(frames[t])
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(out[0].cpu().numpy(), hb[0])
