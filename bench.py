@@ -1,0 +1,482 @@
+#!/usr/bin/env python3
+"""bench.py -- frames/s of the B200 DeltaCNN engine vs dense inference of the same
+network on the same GPU (BASELINE.json metric), with roofline, CPU-oracle baseline,
+end-to-end (host buffers) throughput and clock record.  Prints ONE JSON line.
+
+    python bench.py [--gpus N --steps K --warmup W] [--workload toy|hrnet|yolo]
+    python bench.py --impl reference ...   # the CPU oracle arm (rank 0 only)
+
+A "step" = every stream of this GPU advanced by one frame through the whole hot path
+(input delta -> every layer -> dense output accumulation).  Multi-GPU: one process per
+GPU (torchrun), streams sharded across ranks (weak scaling), NCCL only to gather timings.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import nets  # noqa: E402
+from synth.frames import VideoSpec, Video  # noqa: E402
+
+METRIC = "frames/s per B200 (sparse vs dense same GPU) at update rate; % roofline"
+
+WORKLOADS = {
+    # BASELINE.json configs[1]: 5-layer toy (Fig. 2 shape), 64 ch, 128x128, eps 0.05, ~10 %
+    "toy": dict(cfg="configs[1]", build=lambda dt: nets.toy_net(128, 128, 64, eps=0.05, dtype=dt),
+                video=dict(H=128, W=128, n_blobs=3, blob_h=22, blob_w=22, speed=3, noise_p=0.01),
+                seed=2, S=1, model="toy5 (conv3x3 3-64+ReLU, maxpool2, conv3x3+ReLU, up2, conv3x3)"),
+    # configs[2]: HRNet-W32 256x192 fp16, single stream, eps_in 0.3 + 7 px dilation
+    "hrnet": dict(cfg="configs[2]", build=lambda dt: nets.hrnet_w32(dtype=dt),
+                  video=dict(H=256, W=192, n_blobs=1, blob_h=60, blob_w=24, speed=2, noise_p=0.05),
+                  seed=3, S=1, model="HRNet-W32 pose 256x192"),
+    # configs[3]: YOLOv5s 640x640 fp16, eps_in 0.5 + 7 px dilation, per-layer eps
+    "yolo": dict(cfg="configs[3]", build=lambda dt: nets.yolov5s(dtype=dt),
+                 video=dict(H=640, W=640, n_blobs=20, blob_h=40, blob_w=16, speed=2, noise_p=0.05),
+                 seed=4, S=1, model="YOLOv5s v6 640x640"),
+}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+# ------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------- dense baseline
+def dense_module(net, torch):
+    """PyTorch model of the same layer table (cuDNN dense baseline; never on the engine path)."""
+    import torch.nn.functional as F
+    acts = {"none": lambda t: t, "relu": F.relu, "silu": F.silu, "relu6": F.relu6,
+            "leaky": lambda t: F.leaky_relu(t, 0.1), "sigmoid": torch.sigmoid}
+
+    class Dense(torch.nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.w = torch.nn.ParameterList()
+            self.b = torch.nn.ParameterList()
+            self.idx = {}
+            for i, L in enumerate(net.layers):
+                if L.op == "conv":
+                    self.idx[i] = len(self.w)
+                    self.w.append(torch.nn.Parameter(torch.from_numpy(L.weight).permute(0, 3, 1, 2).contiguous(),
+                                                     requires_grad=False))
+                    self.b.append(torch.nn.Parameter(torch.from_numpy(L.bias), requires_grad=False))
+
+        def forward(self, x):
+            vals = {}
+            for i, L in enumerate(net.layers):
+                xs = [x if j < 0 else vals[j] for j in L.inputs]
+                if L.op == "conv":
+                    k = self.idx[i]
+                    y = acts[L.act](F.conv2d(xs[0], self.w[k], self.b[k], L.stride, L.pad, L.dil, L.groups))
+                elif L.op == "act":
+                    y = acts[L.act](xs[0])
+                elif L.op == "maxpool":
+                    y = F.max_pool2d(xs[0], L.kh, L.stride, L.pad)
+                elif L.op == "avgpool":
+                    y = F.avg_pool2d(xs[0], L.kh, L.stride, L.pad)
+                elif L.op == "up":
+                    y = F.interpolate(xs[0], scale_factor=L.up, mode="nearest")
+                elif L.op == "add":
+                    y = acts[L.act](sum(xs))
+                elif L.op == "concat":
+                    y = torch.cat(xs, 1)
+                else:
+                    raise ValueError(L.op)
+                vals[i] = y
+            return [vals[o] for o in net.outputs]
+    return Dense()
+
+
+# ------------------------------------------------------------------------- helpers
+def make_frames(wl, S, T, rank, dtype):
+    v = wl["video"]
+    vids = [Video(VideoSpec(v["H"], v["W"], 3, v["n_blobs"], v["blob_h"], v["blob_w"], v["speed"],
+                            v["noise_p"], False, wl["seed"] + 1000 * rank + s)) for s in range(S)]
+    return np.stack([np.stack([vv.frame(t, dtype) for vv in vids]) for t in range(T)])
+
+
+def dense_macs(net):
+    """MACs of dense per-frame inference (convs only), per stream."""
+    shape = {-1: (net.in_h, net.in_w, net.in_c)}
+    total = 0
+    for i, L in enumerate(net.layers):
+        H, W, C = shape[L.inputs[0]]
+        if L.op == "conv":
+            Ho = (H + 2 * L.pad - L.dil * (L.kh - 1) - 1) // L.stride + 1
+            Wo = (W + 2 * L.pad - L.dil * (L.kw - 1) - 1) // L.stride + 1
+            total += Ho * Wo * L.c_out * L.kh * L.kw * C // L.groups
+            shape[i] = (Ho, Wo, L.c_out)
+        elif L.op in ("maxpool", "avgpool"):
+            shape[i] = ((H + 2 * L.pad - L.kh) // L.stride + 1, (W + 2 * L.pad - L.kh) // L.stride + 1, C)
+        elif L.op == "up":
+            shape[i] = (H * L.up, W * L.up, C)
+        elif L.op == "concat":
+            shape[i] = (H, W, sum(shape[j][2] for j in L.inputs))
+        else:
+            shape[i] = (H, W, C)
+    return total
+
+
+def cpu_oracle_time(net, frames, budget_s=15.0):
+    """Time the CPU oracle (as it stands) on a bounded prefix of the same clip."""
+    from oracle import DeltaOracle
+    S = frames.shape[1]
+    o = DeltaOracle(net, S, record=False)
+    t0 = time.perf_counter()
+    n = 0
+    for t in range(frames.shape[0]):
+        o.step(frames[t])
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    try:
+        import threadpoolctl
+        info = threadpoolctl.threadpool_info()
+        cores = max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    return n * S / dt, n, cores
+
+
+def flush_l2(buf):
+    buf.add_(1)     # writes > L2 bytes
+
+
+# ------------------------------------------------------------------------- reference arm
+def run_reference(args, wl, rank, world):
+    if rank != 0:
+        return
+    net = wl["build"](args.dtype)
+    S = wl["S"]
+    npdt = np.float16 if args.dtype == "f16" else np.float32
+    T = args.warmup + args.steps
+    frames = make_frames(wl, S, T, 0, npdt)
+    from oracle import DeltaOracle
+    o = DeltaOracle(net, S, record=False)
+    for t in range(args.warmup):
+        o.step(frames[t])
+    t0 = time.perf_counter()
+    for t in range(args.warmup, T):
+        o.step(frames[t])
+    dt = time.perf_counter() - t0
+    try:
+        import threadpoolctl
+        cores = max([i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    v = args.steps * S / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.workload, "baseline_cfg": wl["cfg"],
+                                            "streams": S, "model": wl["model"]},
+            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": cores, "kind": "oracle",
+                             "sample": f"frames {args.warmup}..{T - 1} of the {args.workload} clip "
+                                       f"(numpy fp64 oracle, {S} stream(s))"},
+            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------- engine arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=os.environ.get("DCNN_WORKLOAD", "toy"), choices=list(WORKLOADS))
+    ap.add_argument("--dtype", default="f16", choices=["f16", "f32"])
+    ap.add_argument("--streams", type=int, default=0, help="streams per GPU (default: workload's)")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    wl = WORKLOADS[args.workload]
+    if args.streams:
+        wl = dict(wl, S=args.streams)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        run_reference(args, wl, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2203_03996_b200 import DeltaNet, KCLASS_CONV, KCLASS_TILES, KCLASS_POINTWISE, KCLASS_INPUT
+
+    net = wl["build"](args.dtype)
+    S = wl["S"]
+    npdt = np.float16 if args.dtype == "f16" else np.float32
+    tdt = torch.float16 if args.dtype == "f16" else torch.float32
+    T = args.warmup + args.steps + 1
+    frames_np = make_frames(wl, S, T, rank, npdt)
+    frames = torch.from_numpy(frames_np).cuda()               # inputs resident in HBM
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+
+    eng = DeltaNet(net, n_streams=S, device=local)
+    classes = {"conv": KCLASS_CONV, "tiles": KCLASS_TILES, "pointwise": KCLASS_POINTWISE,
+               "input": KCLASS_INPUT}
+    eng.enable_kernel_timing(KCLASS_CONV | KCLASS_TILES | KCLASS_POINTWISE | KCLASS_INPUT)
+    outs = [torch.empty((S,) + s, dtype=torch.float32, device=dev) for s in eng.out_shapes]
+    l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
+
+    for t in range(args.warmup):
+        eng.process_frame(frames[t], outs, stream)
+    torch.cuda.synchronize()
+
+    dmacs = dense_macs(net) * S
+    kt = {k: [0.0, 0] for k in classes}
+    agg = {"mac_alg": 0, "mac_exec": 0, "tiles": 0, "tiles_proc": 0, "u_in": 0.0, "u_conv": 0.0}
+    conv_ops = [i for i, L in enumerate(net.layers) if L.op == "conv"]
+    step_ms = []
+    clock = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clock.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    for k in range(args.steps):
+        t = args.warmup + k
+        flush_l2(l2)
+        ev0.record(stream)
+        eng.process_frame(frames[t], outs, stream)
+        ev1.record(stream)
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+        for name, c in classes.items():
+            ms, n = eng.kernel_timing(c)
+            kt[name][0] += ms
+            kt[name][1] += n
+        st = eng.stats()["ops"]
+        in_px = S * net.in_h * net.in_w
+        agg["u_in"] += st[0]["active_out"] / in_px
+        dens = []
+        for i in conv_ops:
+            r = st[i + 1]
+            agg["mac_alg"] += r["mac_alg"]
+            agg["mac_exec"] += r["mac_exec"]
+            agg["tiles"] += r["tiles_total"]
+            agg["tiles_proc"] += r["tiles_sparse"] + r["tiles_dense"]
+            Hs, Ws, _ = eng.op_shape(net.layers[i].inputs[0])
+            dens.append(r["active_in"] / (S * Hs * Ws))
+        agg["u_conv"] += float(np.mean(dens))
+    torch.cuda.synchronize()
+    clocks = clock.stop()
+    total_ms = float(np.sum(step_ms))
+    if dist:
+        tt = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    frames_all = S * world * args.steps
+    value = frames_all / (total_ms / 1e3)
+
+    # --- roofline of the dominant kernel class (delta conv) ---------------------
+    pk = peaks()
+    conv_ms, conv_n = kt["conv"]
+    alg_flops = 2.0 * agg["mac_alg"]
+    per_launch_flops = alg_flops / max(1, conv_n)
+    avg_launch_s = conv_ms / 1e3 / max(1, conv_n)
+    tc = False
+    if tc:
+        peak = pk["bf16_tflops_sustained"]
+        bound, unit = "tensor", "TFLOP/s"
+    else:
+        # CUDA-core FFMA: 148 SMs x 128 fp32 lanes x 2 FLOP x max SM clock
+        peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        bound, unit = "alu", "TFLOP/s"
+    achieved = per_launch_flops / avg_launch_s / 1e12 if avg_launch_s > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.workload, {}).get("conv_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                "frac": achieved / peak if peak else None, "traffic": traffic,
+                "kernel": "delta conv (k_conv_cc)",
+                "peak_source": "148 SM x 128 FFMA lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)"}
+
+    # --- e2e through the C ABI with host buffers --------------------------------
+    eng2 = DeltaNet(net, n_streams=S, device=local)
+    host_frames = torch.from_numpy(frames_np).pin_memory()
+    host_outs = [torch.empty((S,) + s, dtype=torch.float32).pin_memory() for s in eng2.out_shapes]
+    hf = [host_frames[t].numpy() for t in range(T)]
+    ho = [o.numpy() for o in host_outs]
+    for t in range(args.warmup):
+        eng2.process_frame_host(hf[t], ho, stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(args.steps):
+        eng2.process_frame_host(hf[args.warmup + k], ho, stream)
+    e1.record(stream)
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e = {"value": frames_all / (e2e_ms / 1e3), "unit": "frames/s",
+           "h2d_bytes_per_step": int(frames_np[0].nbytes),
+           "d2h_bytes_per_step": int(sum(o.nbytes for o in ho))}
+    eng2.close()
+
+    # --- dense baseline: PyTorch/cuDNN fp16 channels_last, CUDA graph, same S ---
+    dense = None
+    if not args.no_dense:
+        torch.backends.cudnn.benchmark = True
+        model = dense_module(net, torch).to(dev, tdt).to(memory_format=torch.channels_last)
+        xin = frames[:, :, :, :, :].permute(0, 1, 4, 2, 3)       # [T,S,C,H,W] view
+        static_x = xin[0].contiguous(memory_format=torch.channels_last)
+        with torch.no_grad():
+            for _ in range(3):
+                model(static_x)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                static_out = model(static_x)
+            dms = []
+            for k in range(args.steps):
+                static_x.copy_(xin[args.warmup + k])
+                flush_l2(l2)
+                ev0.record(stream)
+                g.replay()
+                ev1.record(stream)
+                ev1.synchronize()
+                dms.append(ev0.elapsed_time(ev1))
+        dense_fps = S * args.steps / (np.sum(dms) / 1e3)
+        # deviation of the sparse engine from dense inference at the last timed frame
+        eng_last = [o.cpu().double() for o in outs]
+        static_x.copy_(xin[args.warmup + args.steps - 1])
+        g.replay()
+        torch.cuda.synchronize()
+        dev_max = 0.0
+        for a, b in zip(eng_last, static_out):
+            bb = b.float().permute(0, 2, 3, 1).cpu().double()
+            dev_max = max(dev_max, float((a - bb).abs().max() / bb.abs().max().clamp_min(1e-12)))
+        dense = {"fps": dense_fps, "ms_per_step": float(np.mean(dms)), "speedup": value / world / dense_fps,
+                 "deviation_vs_dense": dev_max, "impl": "torch cuDNN fp16 channels_last + CUDA graph"}
+
+    # --- CPU oracle baseline (rank 0, N=1) ------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        fps, n, cores = cpu_oracle_time(net, frames_np[: min(T, 40)])
+        cpu = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle",
+               "sample": f"first {n} frames of the {args.workload} clip ({S} stream(s)), numpy fp64 oracle"}
+
+    kpf = eng.kernels_per_frame()
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic",
+        "config": {"workload": args.workload, "baseline_cfg": wl["cfg"], "model": wl["model"],
+                   "streams_per_gpu": S, "frame": [net.in_h, net.in_w, 3],
+                   "input_eps": net.input_eps, "input_dilation": net.input_dilation,
+                   "inner_eps": max([L.eps for L in net.layers if L.truncates] + [0]),
+                   "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"streams x{world}"},
+        "update": {"u_in": agg["u_in"] / args.steps, "u_conv": agg["u_conv"] / args.steps,
+                   "mac_frac": agg["mac_alg"] / (dmacs * args.steps),
+                   "mac_exec_frac": agg["mac_exec"] / (dmacs * args.steps),
+                   "tiles_processed_frac": agg["tiles_proc"] / max(1, agg["tiles"])},
+        "dense": dense,
+        "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": kpf * args.steps,
+        "kernels_per_frame": kpf,
+        "clocks": clocks,
+        "p50_ms": float(np.percentile(step_ms, 50)), "p99_ms": float(np.percentile(step_ms, 99)),
+    }
+    eng.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

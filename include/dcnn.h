@@ -175,6 +175,25 @@ DCNN_API dcnn_status dcnn_get_stats(dcnn_net* net, dcnn_op_stats* per_op, int64_
 DCNN_API dcnn_status dcnn_debug_read(dcnn_net* net, int32_t op, int32_t which, void* host,
                             int64_t* bytes);
 
+/* Kernel classes for timing (bit mask). */
+enum { DCNN_KCLASS_CONV = 1,       /* delta-conv compute kernels (a3/a4)              */
+       DCNN_KCLASS_TILES = 2,      /* mask -> tile compaction (a2)                    */
+       DCNN_KCLASS_POINTWISE = 4,  /* act/pool/add/concat/up/affine (a5-a7)           */
+       DCNN_KCLASS_INPUT = 8 };    /* delta generation (a1)                            */
+
+/* Profiling: record CUDA events around every kernel of the classes in mask.
+ * Must be called before the first process_frame (it shapes the frame graph). */
+DCNN_API dcnn_status dcnn_enable_kernel_timing(dcnn_net* net, int32_t class_mask);
+
+/* Summed device time (ms) and launch count of one kernel class in the most
+ * recent frame.  Synchronises the stream of the last process_frame. */
+DCNN_API dcnn_status dcnn_kernel_timing(dcnn_net* net, int32_t kernel_class, float* ms,
+                                        int32_t* launches);
+
+/* Debug poisoning: fill every delta buffer with NaN so
+ * that any read of a masked-off (stale) value would surface in the outputs. */
+DCNN_API dcnn_status dcnn_debug_poison(dcnn_net* net);
+
 /* Number of kernel launches enqueued by one process_frame (graph nodes). */
 DCNN_API int32_t dcnn_kernels_per_frame(dcnn_net* net);
 

@@ -16,6 +16,7 @@ BUF_DELTA, BUF_MASK, BUF_XA, BUF_XT, BUF_OUT, BUF_POOLA = range(6)
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_UNSUPPORTED", 4: "ERR_NONFINITE",
           5: "ERR_CUDA", 6: "ERR_OOM"}
 FLAG_NO_TENSOR_CORES = 1
+KCLASS_CONV, KCLASS_TILES, KCLASS_POINTWISE, KCLASS_INPUT = 1, 2, 4, 8
 
 
 class dcnn_layer_desc(C.Structure):
@@ -74,9 +75,13 @@ def load_library(path: str = LIB_PATH):
     lib.dcnn_kernels_per_frame.argtypes = [vp]
     lib.dcnn_kernels_per_frame.restype = C.c_int32
     lib.dcnn_last_error.restype = C.c_char_p
+    lib.dcnn_enable_kernel_timing.argtypes = [vp, C.c_int32]
+    lib.dcnn_kernel_timing.argtypes = [vp, C.c_int32, C.POINTER(C.c_float), C.POINTER(C.c_int32)]
+    lib.dcnn_debug_poison.argtypes = [vp]
     for name in ["dcnn_create_net", "dcnn_set_threshold", "dcnn_process_frame",
                  "dcnn_process_frame_host", "dcnn_reset", "dcnn_op_shape", "dcnn_get_stats",
-                 "dcnn_debug_read"]:
+                 "dcnn_debug_read", "dcnn_enable_kernel_timing", "dcnn_kernel_timing",
+                 "dcnn_debug_poison"]:
         getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -203,6 +208,17 @@ class DeltaNet:
         _check(self.lib, self.lib.dcnn_debug_read(self.h, op, which, C.c_void_p(out.ctypes.data),
                                                   C.byref(nb)))
         return out
+
+    def enable_kernel_timing(self, class_mask: int):
+        _check(self.lib, self.lib.dcnn_enable_kernel_timing(self.h, class_mask))
+
+    def kernel_timing(self, kclass: int):
+        ms, n = C.c_float(), C.c_int32()
+        _check(self.lib, self.lib.dcnn_kernel_timing(self.h, kclass, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def debug_poison(self):
+        _check(self.lib, self.lib.dcnn_debug_poison(self.h))
 
     def kernels_per_frame(self):
         return self.lib.dcnn_kernels_per_frame(self.h)

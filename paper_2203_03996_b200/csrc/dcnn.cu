@@ -97,6 +97,10 @@ struct dcnn_net {
   // host staging for the _host entry point
   void* h_frames = nullptr;
   size_t frame_bytes = 0;
+  // kernel timing (profiling)
+  int timing_mask = 0;
+  struct Timed { int cls; cudaEvent_t a, b; };
+  std::vector<Timed> timed;
 };
 
 template <typename T>
@@ -133,7 +137,7 @@ static dcnn_status plan_cc(Op& o) {
 }
 
 static size_t cc_smem(const Op& o) {
-  return (size_t)o.WH * o.WW * o.CIC * 4 + ((size_t)o.WH * o.WW + 15) / 16 * 16 +
+  return ((size_t)o.WH * o.WW * o.CIC * 4 + 15) / 16 * 16 + ((size_t)o.WH * o.WW + 15) / 16 * 16 +
          (size_t)o.STH * o.STW * o.Cp * 4;
 }
 
@@ -155,6 +159,26 @@ static Epi make_epi(dcnn_net* n, int i) {
   return e;
 }
 
+// Event pair around one kernel launch when its class is being timed.
+struct TimeScope {
+  dcnn_net* n;
+  cudaStream_t st;
+  int idx = -1;
+  TimeScope(dcnn_net* n_, cudaStream_t st_, int cls) : n(n_), st(st_) {
+    if (!(n->timing_mask & cls)) return;
+    dcnn_net::Timed t;
+    t.cls = cls;
+    cudaEventCreate(&t.a);
+    cudaEventCreate(&t.b);
+    idx = (int)n->timed.size();
+    n->timed.push_back(t);
+    cudaEventRecordWithFlags(t.a, st, cudaEventRecordExternal);
+  }
+  ~TimeScope() {
+    if (idx >= 0) cudaEventRecordWithFlags(n->timed[idx].b, st, cudaEventRecordExternal);
+  }
+};
+
 static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
   int k = 0;
   const int nops = (int)n->ops.size();
@@ -164,7 +188,10 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
   ip.S = n->S; ip.H = n->inH; ip.W = n->inW; ip.C = n->inC; ip.radius = n->radius;
   ip.frame = n->frame_in; ip.P = n->P; ip.delta = n->in_delta; ip.mask = n->in_mask;
   ip.eps = n->eps; ip.first = n->first; ip.err = n->err; ip.n_active = n->stats + 1;
-  launch_input(ip, n->dtype, st);
+  {
+    TimeScope ts(n, st, DCNN_KCLASS_INPUT);
+    launch_input(ip, n->dtype, st);
+  }
   ++k;
   auto src_delta = [&](int j) -> const void* { return j < 0 ? n->in_delta : n->ops[j].delta; };
   auto src_mask = [&](int j) -> const uint8_t* { return j < 0 ? n->in_mask : n->ops[j].mask; };
@@ -180,7 +207,10 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       tp.list_cc = o.list_cc; tp.count_cc = n->counts + o.cnt_idx;
       tp.list_tc = o.list_tc; tp.count_tc = n->counts + o.cnt_idx + 1;
       tp.stats = n->stats + (size_t)(i + 1) * 8;
-      launch_tiles(tp, st);
+      {
+        TimeScope ts(n, st, DCNN_KCLASS_TILES);
+        launch_tiles(tp, st);
+      }
       ++k;
       ConvCCParams cp;
       cp.S = n->S; cp.H = o.Hi; cp.W = o.Wi; cp.Ci = o.Ci;
@@ -192,7 +222,10 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       cp.wt = o.wt; cp.bias = o.bias;
       cp.list = o.list_cc; cp.count = n->counts + o.cnt_idx;
       cp.ep = make_epi(n, i);
-      launch_conv_cc(cp, n->dtype, o.grid_cc, st);
+      {
+        TimeScope ts(n, st, DCNN_KCLASS_CONV);
+        launch_conv_cc(cp, n->dtype, o.grid_cc, st);
+      }
       ++k;
     } else {
       PwParams pp;
@@ -207,9 +240,13 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       pp.k = o.kh; pp.stride = o.stride; pp.pad = o.pad; pp.up = o.up;
       pp.scale = o.scale; pp.shift = o.shift; pp.poolA = o.poolA;
       pp.ep = make_epi(n, i);
-      launch_pointwise(pp, n->dtype, st);
+      {
+        TimeScope ts(n, st, DCNN_KCLASS_POINTWISE);
+        launch_pointwise(pp, n->dtype, st);
+      }
       ++k;
       if (o.kind == DCNN_OP_MAXPOOL) {
+        TimeScope ts(n, st, DCNN_KCLASS_POINTWISE);
         launch_pool_update(pp, n->dtype, st);
         ++k;
       }
@@ -244,6 +281,10 @@ void dcnn_destroy_net(dcnn_net* n) {
   if (n->cap) cudaStreamDestroy(n->cap);
   for (void* p : n->allocs) cudaFree(p);
   if (n->err_host) cudaFreeHost(n->err_host);
+  for (auto& t : n->timed) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
   if (n->h_frames) cudaFreeHost(n->h_frames);
   delete n;
 }
@@ -606,6 +647,43 @@ dcnn_status dcnn_debug_read(dcnn_net* n, int32_t op, int32_t which, void* host, 
     CUDA_TRY(cudaDeviceSynchronize());
     CUDA_TRY(cudaMemcpy(host, src, nb, cudaMemcpyDeviceToHost));
   }
+  return DCNN_OK;
+}
+
+dcnn_status dcnn_enable_kernel_timing(dcnn_net* n, int32_t class_mask) {
+  if (!n) return fail(DCNN_ERR_ARG, "null net");
+  if (n->exec) return fail(DCNN_ERR_ARG, "timing must be enabled before the first process_frame");
+  n->timing_mask = class_mask;
+  return DCNN_OK;
+}
+
+dcnn_status dcnn_kernel_timing(dcnn_net* n, int32_t cls, float* ms, int32_t* launches) {
+  if (!n || !ms || !launches) return fail(DCNN_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(n->device));
+  CUDA_TRY(cudaStreamSynchronize(n->last));
+  float tot = 0.f;
+  int cnt = 0;
+  for (auto& t : n->timed) {
+    if (t.cls != cls) continue;
+    float e = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&e, t.a, t.b));
+    tot += e;
+    ++cnt;
+  }
+  *ms = tot;
+  *launches = cnt;
+  return DCNN_OK;
+}
+
+dcnn_status dcnn_debug_poison(dcnn_net* n) {
+  if (!n) return fail(DCNN_ERR_ARG, "null net");
+  CUDA_TRY(cudaSetDevice(n->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  const size_t es = n->esz;
+  CUDA_TRY(cudaMemset(n->in_delta, 0xFF, (size_t)n->S * n->inH * n->inW * n->inC * es));
+  for (auto& o : n->ops)
+    CUDA_TRY(cudaMemset(o.delta, 0xFF, (size_t)n->S * o.H * o.W * o.C * es));
+  CUDA_TRY(cudaDeviceSynchronize());
   return DCNN_OK;
 }
 

@@ -88,7 +88,7 @@ constexpr int CC_THREADS = 256;
 constexpr int CC_MAXPPT = 8;
 
 size_t conv_cc_smem(const ConvCCParams& p) {
-  const size_t win = (size_t)p.WH * p.WW * p.CIC * sizeof(float);
+  const size_t win = ((size_t)p.WH * p.WW * p.CIC * sizeof(float) + 15) / 16 * 16;
   const size_t msk = ((size_t)p.WH * p.WW + 15) / 16 * 16;
   const size_t zt = (size_t)p.STH * p.STW * p.Cp * sizeof(float);
   return win + msk + zt;
@@ -98,7 +98,7 @@ template <typename T>
 __global__ void __launch_bounds__(CC_THREADS) k_conv_cc(ConvCCParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   float* win = reinterpret_cast<float*>(smem);
-  uint8_t* wmask = smem + (size_t)p.WH * p.WW * p.CIC * sizeof(float);
+  uint8_t* wmask = smem + ((size_t)p.WH * p.WW * p.CIC * sizeof(float) + 15) / 16 * 16;
   float* zt = reinterpret_cast<float*>(wmask + ((size_t)p.WH * p.WW + 15) / 16 * 16);
   const T* din = reinterpret_cast<const T*>(p.delta_in);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -142,10 +142,14 @@ def test_per_stream_reset_and_nan_poison():
         if t == 5:
             eng.reset(1)
             orc.reset(1)
+        if t > 0:
+            eng.debug_poison()           # every stale delta is NaN from here on
         eng.process_frame(torch.from_numpy(frames[t]).cuda(), out)
         want = orc.step(frames[t])
         torch.cuda.synchronize()
-        assert max_abs_rel(out[0].cpu().numpy(), want[0]) <= 1e-4
+        g = out[0].cpu().numpy()
+        assert np.isfinite(g).all()
+        assert max_abs_rel(g, want[0]) <= 1e-4
     eng.close()
 
 
