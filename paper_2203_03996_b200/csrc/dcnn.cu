@@ -61,6 +61,11 @@ struct Op {
   int* list_tc = nullptr;
   int cnt_idx = -1;                 // index into counts[] (2 ints per conv)
   int grid_cc = 0;
+  // tensor-core path (a3)
+  bool tc = false;
+  ConvTCParams tcp;
+  __half* wtc = nullptr;
+  int grid_tc = 0;
   // affine
   float* scale = nullptr;
   float* shift = nullptr;
@@ -136,6 +141,44 @@ static dcnn_status plan_cc(Op& o) {
   return DCNN_OK;
 }
 
+static bool plan_tc(Op& o, int dtype, int flags) {
+  if (dtype != DCNN_F16 || (flags & DCNN_FLAG_NO_TENSOR_CORES)) return false;
+  if (o.Ci % 16 || o.C > 512) return false;
+  ConvTCParams& p = o.tcp;
+  memset(&p, 0, sizeof(p));
+  p.Np = (o.C + 15) / 16 * 16;
+  p.n_acc = p.Np <= 256 ? 2 : 1;
+  p.acc_stride = p.n_acc == 2 ? (p.Np + 31) / 32 * 32 : 0;
+  int cols = p.n_acc == 2 ? 2 * p.acc_stride : 512;
+  int tc = 32;
+  while (tc < cols) tc *= 2;
+  p.tmem_cols = tc;
+  const int s = o.stride, d = o.dil;
+  p.HH = 15 * s + (o.kh - 1) * d + 1;
+  p.WW = 7 * s + (o.kw - 1) * d + 1;
+  const int WQ = (p.WW + s - 1) / s;
+  p.WWp = s * WQ;
+  const size_t budget = 227 * 1024 - 384;
+  for (int BK = 64; BK >= 16; BK /= 2) {
+    if (o.Ci % BK) continue;
+    const int plane = (p.HH * p.WWp * 16 + 127) / 128 * 128 + 16;
+    const int a_bytes = ((BK / 8) * plane + 127) / 128 * 128;
+    const int b_bytes = p.Np * BK * 2;
+    if (2 * (size_t)a_bytes + 2 * (size_t)b_bytes > budget) continue;
+    int stages = (int)((budget - 2 * (size_t)a_bytes) / b_bytes);
+    if (stages > 8) stages = 8;
+    if ((p.stride * p.WWp * 16) >> 4 >= (1 << 14) || plane >> 4 >= (1 << 14)) continue;
+    p.BK = BK;
+    p.ncb = o.Ci / BK;
+    p.plane = plane;
+    p.a_bytes = a_bytes;
+    p.b_bytes = b_bytes;
+    p.stages = stages;
+    return true;
+  }
+  return false;
+}
+
 static size_t cc_smem(const Op& o) {
   return ((size_t)o.WH * o.WW * o.CIC * 4 + 15) / 16 * 16 + ((size_t)o.WH * o.WW + 15) / 16 * 16 +
          (size_t)o.STH * o.STW * o.Cp * 4;
@@ -203,7 +246,7 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       tp.kh = o.kh; tp.kw = o.kw; tp.stride = o.stride; tp.pad = o.pad; tp.dil = o.dil;
       tp.TH = o.TH; tp.TW = o.TW; tp.nty = o.nty; tp.ntx = o.ntx;
       tp.mask_in = src_mask(o.in[0]); tp.mconv = o.mask; tp.first = n->first;
-      tp.sparse_max = 4; tp.use_tc = 0;
+      tp.sparse_max = 4; tp.use_tc = o.tc ? 1 : 0;
       tp.list_cc = o.list_cc; tp.count_cc = n->counts + o.cnt_idx;
       tp.list_tc = o.list_tc; tp.count_tc = n->counts + o.cnt_idx + 1;
       tp.stats = n->stats + (size_t)(i + 1) * 8;
@@ -227,6 +270,17 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
         launch_conv_cc(cp, n->dtype, o.grid_cc, st);
       }
       ++k;
+      if (o.tc) {
+        ConvTCParams p = o.tcp;
+        p.delta_in = reinterpret_cast<const __half*>(src_delta(o.in[0]));
+        p.mask_in = src_mask(o.in[0]);
+        p.list = o.list_tc;
+        p.count = n->counts + o.cnt_idx + 1;
+        p.ep = make_epi(n, i);
+        TimeScope ts(n, st, DCNN_KCLASS_CONV);
+        launch_conv_tc(p, o.grid_tc, st);
+        ++k;
+      }
     } else {
       PwParams pp;
       memset(&pp, 0, sizeof(pp));
@@ -434,6 +488,8 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
     }
     if (o.kind == DCNN_OP_CONV) {
       if ((r = plan_cc(o))) return r;
+      o.tc = plan_tc(o, n->dtype, n->flags);
+      if (o.tc) { o.TH = 16; o.TW = 8; }
       o.K = o.kh * o.kw * (o.Ci / o.groups);
       o.nty = (o.H + o.TH - 1) / o.TH;
       o.ntx = (o.W + o.TW - 1) / o.TW;
@@ -466,6 +522,30 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
       CUDA_TRY(cudaMemcpy(o.bias, b.data(), o.C * 4, cudaMemcpyHostToDevice));
       const size_t smem = cc_smem(o);
       if (smem > 200 * 1024) return fail(DCNN_ERR_UNSUPPORTED, "conv tile does not fit shared memory");
+      if (o.tc) {
+        ConvTCParams& p = o.tcp;
+        p.S = n->S; p.H = o.Hi; p.W = o.Wi; p.Ci = o.Ci; p.Ho = o.H; p.Wo = o.W; p.Co = o.C;
+        p.kh = o.kh; p.kw = o.kw; p.stride = o.stride; p.pad = o.pad; p.dil = o.dil;
+        p.nty = o.nty; p.ntx = o.ntx;
+        p.bias = o.bias;
+        // weights -> the shared-memory image of every (channel block, tap) step:
+        // [ncb*kh*kw][BK/8][Np][8] fp16, K-major core matrices (8 rows x 16 B)
+        const int ntaps = o.kh * o.kw, nch = p.BK / 8;
+        std::vector<__half> w((size_t)p.ncb * ntaps * nch * p.Np * 8, __float2half(0.f));
+        for (int cb = 0; cb < p.ncb; ++cb)
+          for (int tap = 0; tap < ntaps; ++tap)
+            for (int ch = 0; ch < nch; ++ch)
+              for (int nn = 0; nn < o.C; ++nn)
+                for (int e = 0; e < 8; ++e) {
+                  const int ci = cb * p.BK + ch * 8 + e;
+                  const float v = wt[((size_t)tap * o.Ci + ci) * o.Cp + nn];   // dense-expanded groups
+                  w[((((size_t)(cb * ntaps + tap) * nch + ch) * p.Np + nn) * 8) + e] = __float2half_rn(v);
+                }
+        if ((r = dalloc(n, &o.wtc, w.size() * 2))) return r;
+        CUDA_TRY(cudaMemcpy(o.wtc, w.data(), w.size() * 2, cudaMemcpyHostToDevice));
+        p.wtc = o.wtc;
+        o.grid_tc = std::max(1, std::min(n->S * o.nty * o.ntx, 148));
+      }
     }
     if (o.kind == DCNN_OP_AFFINE) {
       if ((r = dalloc(n, &o.scale, o.C * 4))) return r;
@@ -475,6 +555,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
     }
   }
   CUDA_TRY(conv_cc_init());
+  CUDA_TRY(conv_tc_init());
   CUDA_TRY(cudaStreamCreateWithFlags(&n->cap, cudaStreamNonBlocking));
   CUDA_TRY(cudaDeviceSynchronize());
   return DCNN_OK;

@@ -61,6 +61,29 @@ void launch_conv_cc(const ConvCCParams& p, int dtype, int grid, cudaStream_t st)
 size_t conv_cc_smem(const ConvCCParams& p);
 cudaError_t conv_cc_init();     // once per process/device: raise the dynamic smem limit
 
+// ---------------------------------------------------------------- a3: tensor-core conv
+struct ConvTCParams {
+  int S, H, W, Ci;
+  int Ho, Wo, Co, Np;           // Np: C_out padded to a multiple of 16
+  int kh, kw, stride, pad, dil;
+  int nty, ntx;                 // 16x8 output tiles
+  int HH, WW, WWp;              // halo rows, cols, padded cols (multiple of stride)
+  int BK, ncb;                  // input channels per block, number of blocks
+  int plane;                    // bytes per 8-channel plane of the halo buffer (= LBO of A)
+  int a_bytes, b_bytes, stages; // halo buffer bytes, weight stage bytes, weight ring depth
+  int n_acc, acc_stride;        // TMEM accumulators and their column stride
+  int tmem_cols;
+  const __half* delta_in;
+  const uint8_t* mask_in;
+  const __half* wtc;            // [ncb*kh*kw][BK/8][Np][8] fp16 (smem image of each step)
+  const float* bias;
+  const int* list; const int* count;
+  Epi ep;
+};
+size_t conv_tc_smem(const ConvTCParams& p);
+cudaError_t conv_tc_init();
+void launch_conv_tc(const ConvTCParams& p, int grid, cudaStream_t st);
+
 // ---------------------------------------------------------------- a6/a7 pointwise ops
 struct PwParams {
   int kind;                     // dcnn_op
