@@ -96,7 +96,9 @@ typedef struct {
 } dcnn_layer_desc;
 
 enum {
-  DCNN_FLAG_NO_TENSOR_CORES = 1   /* route every conv through the CUDA-core kernel      */
+  DCNN_FLAG_NO_TENSOR_CORES = 1,  /* route every conv through the CUDA-core kernel      */
+  DCNN_FLAG_FP32_CACHES = 2       /* dtype F16: keep x^A, x^T and pool accumulators in
+                                     fp32 (deltas stay fp16)                             */
 };
 
 typedef struct {
@@ -170,7 +172,8 @@ DCNN_API dcnn_status dcnn_get_stats(dcnn_net* net, dcnn_op_stats* per_op, int64_
                            int32_t* device_error);
 
 /* Copy one internal buffer of op (-1 = input layer) to host memory (all streams):
- * DELTA/XA/XT/POOLA in dtype, MASK u8, OUT fp32.  Synchronises the device.
+ * DELTA in dtype, XA/XT/POOLA in the cache dtype (dtype, or fp32 with
+ * DCNN_FLAG_FP32_CACHES; the input layer's XA is P, in dtype), MASK u8, OUT fp32.  Synchronises the device.
  * bytes receives the buffer size; host may be NULL to query the size only. */
 DCNN_API dcnn_status dcnn_debug_read(dcnn_net* net, int32_t op, int32_t which, void* host,
                             int64_t* bytes);

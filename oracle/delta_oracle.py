@@ -204,10 +204,13 @@ class DeltaOracle:
       first[s]   stream s runs its next frame densely (frame 0 or after reset)
     """
 
-    def __init__(self, net, n_streams=1, storage=None, record=True):
+    def __init__(self, net, n_streams=1, storage=None, record=True, cache_storage=None):
         self.net = net
         self.S = n_streams
         self.dt = storage or net.dtype
+        # caches x^A, x^T and pool accumulators (PAPER.md:389 "memory overhead of weights
+        # and caches"): the net's cache dtype unless overridden
+        self.cdt = cache_storage or (None if storage else getattr(net, "cache_dtype", None)) or self.dt
         self.record = record
         self.P = None
         self.A, self.T, self.O = {}, {}, {}
@@ -228,6 +231,9 @@ class DeltaOracle:
 
     def _q(self, x):
         return quantize(x, self.dt)
+
+    def _qc(self, x):
+        return quantize(x, self.cdt)
 
     def _truncate(self, i, z, m_in, eps, f, first):
         """Fused activation + truncation, PAPER.md:205-227 (Eqs. 4-6), Fig. 3.
@@ -250,9 +256,9 @@ class DeltaOracle:
         upd = m_in & (fb | (eps < 0) | (dmax > eps))            # Z1 strict, Z22
         trn = m_in & ~upd
         # updated pixels: x^A := x^A + x^T + dx (Eq. 6), x^T := 0
-        self.A[i] = np.where(upd[..., None], self._q(s), np.where(fb[..., None], 0.0, A))
+        self.A[i] = np.where(upd[..., None], self._qc(s), np.where(fb[..., None], 0.0, A))
         self.T[i] = np.where(upd[..., None], 0.0,
-                             np.where(trn[..., None], self._q(T_eff + z), T_eff))
+                             np.where(trn[..., None], self._qc(T_eff + z), T_eff))
         dout = np.where(upd[..., None], self._q(d), 0.0)
         return dout, upd
 
@@ -339,7 +345,7 @@ class DeltaOracle:
                 mo = mask_conv(mi, L.kh, L.kw, L.stride, L.pad, 1) | fb
                 d = np.where(mo[..., None],
                              self._q(maxpool2d(A_new, L.kh, L.stride, L.pad) - prev), 0.0)
-                self.A[i] = np.where(mi[..., None], self._q(A_new), A_old)
+                self.A[i] = np.where(mi[..., None], self._qc(A_new), A_old)
             elif L.op == "avgpool":
                 dx, mi = ins[0]
                 dxm = np.where(mi[..., None], dx, 0.0)

@@ -16,6 +16,7 @@ BUF_DELTA, BUF_MASK, BUF_XA, BUF_XT, BUF_OUT, BUF_POOLA = range(6)
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_UNSUPPORTED", 4: "ERR_NONFINITE",
           5: "ERR_CUDA", 6: "ERR_OOM"}
 FLAG_NO_TENSOR_CORES = 1
+FLAG_FP32_CACHES = 2
 KCLASS_CONV, KCLASS_TILES, KCLASS_POINTWISE, KCLASS_INPUT = 1, 2, 4, 8
 
 
@@ -115,6 +116,9 @@ class DeltaNet:
         self.net = net
         self.S = n_streams
         self.dtype = net.dtype
+        self.cache_dtype = getattr(net, "cache_dtype", None) or net.dtype
+        if self.dtype == "f16" and self.cache_dtype == "f32":
+            flags |= FLAG_FP32_CACHES
         self._keep = []
         L = len(net.layers)
         arr = (dcnn_layer_desc * L)()
@@ -201,7 +205,9 @@ class DeltaNet:
         elif which == BUF_POOLA:
             Ly = self.net.layers[op]
             Hi, Wi, Ci = self.op_shape(Ly.inputs[0])
-            out = np.empty((self.S, Hi, Wi, Ci), np.float16 if self.dtype == "f16" else np.float32)
+            out = np.empty((self.S, Hi, Wi, Ci), np.float16 if self.cache_dtype == "f16" else np.float32)
+        elif which in (BUF_XA, BUF_XT) and op >= 0:
+            out = np.empty((self.S, H, W, Cc), np.float16 if self.cache_dtype == "f16" else np.float32)
         else:
             out = np.empty((self.S, H, W, Cc), np.float16 if self.dtype == "f16" else np.float32)
         assert out.nbytes == nb.value, (out.nbytes, nb.value)

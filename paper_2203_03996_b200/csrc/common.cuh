@@ -1,9 +1,10 @@
 // common.cuh -- device helpers shared by the DeltaCNN sm_100a kernels.
 //
-// Storage types: every delta map, cache (x^A, x^T, pool accumulators) and
-// frame is stored in the net dtype T (float or __half); every computation is
-// done in fp32 (fp32 on the desktop GPUs, fp16 storage on
-// Jetson Nano "to reduce memory overhead of weights and caches").
+// Types: every delta map and frame is stored in the net dtype T (float or
+// __half); the caches x^A, x^T and the max-pool accumulators are stored in the
+// cache type TC (= T by default, fp32 with DCNN_FLAG_FP32_CACHES); every
+// computation is done in fp32 (fp32 on the desktop GPUs,
+// fp16 storage on Jetson Nano "to reduce memory overhead of weights and caches").
 #pragma once
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -22,6 +23,39 @@ template <typename T> __device__ __forceinline__ float rnd(float v);
 template <> __device__ __forceinline__ float rnd<float>(float v) { return v; }
 template <> __device__ __forceinline__ float rnd<__half>(float v) {
   return __half2float(__float2half_rn(v));
+}
+
+// 8 consecutive channels (16 B of fp16 / 32 B of fp32), p aligned accordingly
+__device__ __forceinline__ void ld8(const __half* p, float v[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __half22float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void ld8(const float* p, float v[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0];
+  const float4 b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void st8(__half* p, const float v[8]) {
+  uint4 u;
+  __half2* h = reinterpret_cast<__half2*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ void st8(float* p, const float v[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void st8_zero(__half* p) { *reinterpret_cast<uint4*>(p) = make_uint4(0, 0, 0, 0); }
+__device__ __forceinline__ void st8_zero(float* p) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+  reinterpret_cast<float4*>(p)[1] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // activation f of Eq. 5 (PAPER.md:182-184 for ReLU)
@@ -54,8 +88,8 @@ struct Epi {
   int act;                     // dcnn_act; != NONE => truncation point (Eqs. 4-6)
   float act_param;
   const float* eps;            // device slot of this op's threshold
-  void* xA;                    // [S,H,W,C] accumulated values x^A (T)
-  void* xT;                    // [S,H,W,C] truncated values x^T  (T)
+  void* xA;                    // [S,H,W,C] accumulated values x^A (TC)
+  void* xT;                    // [S,H,W,C] truncated values x^T  (TC)
   void* delta;                 // [S,H,W,C] delta out (T)
   uint8_t* mask;               // [S,H,W]  mask out
   float* O;                    // [S,H,W,C] dense output accumulation (fp32) or null
@@ -69,9 +103,9 @@ constexpr int MAXK = 16;       // channels per lane in a warp epilogue: C <= 512
 // One warp finishes one output pixel whose pre-activation delta z (fp32, bias
 // included on the first frame) is produced by zf(c).  Implements PAPER.md
 // §3.1 "Truncating small updates" (Eqs. 4-6) when e.act != NONE, else emits z.
-// Writes delta, caches, mask and the output accumulation; lanes stride channels.
+// Scalar channel access (any C); used when C is not a multiple of 8.
 // Returns the pixel's output mask bit (warp-uniform).
-template <typename T, typename ZF>
+template <typename T, typename TC, typename ZF>
 __device__ __forceinline__ bool warp_finish_pixel(const Epi& e, long long pix, int lane, ZF zf) {
   const int C = e.C;
   const int s = (int)(pix / e.HW);
@@ -80,8 +114,8 @@ __device__ __forceinline__ bool warp_finish_pixel(const Epi& e, long long pix, i
   float* O = e.O ? e.O + pix * C : nullptr;
   bool upd = true;
   if (e.act != ACT_NONE) {
-    T* A = reinterpret_cast<T*>(e.xA) + pix * C;
-    T* Tt = reinterpret_cast<T*>(e.xT) + pix * C;
+    TC* A = reinterpret_cast<TC*>(e.xA) + pix * C;
+    TC* Tt = reinterpret_cast<TC*>(e.xT) + pix * C;
     float zv[MAXK], tv[MAXK], sv[MAXK], dv[MAXK];
     float mx = 0.f;
 #pragma unroll
@@ -127,9 +161,116 @@ __device__ __forceinline__ bool warp_finish_pixel(const Epi& e, long long pix, i
   return upd;
 }
 
+// Group of G lanes (power of two, aligned inside the warp) finishes one pixel;
+// each lane owns 8-channel chunks j = gl, gl+G, ... (C % 8 == 0, C <= 512 when
+// truncating, so at most 2 chunks per lane when G = min(32, pow2 <= C/8)).
+// zf(j, z[8]) produces the pre-activation delta of chunk j.  All lanes of the
+// warp must call this together (shuffle reduction).
+template <typename T, typename TC, typename ZF>
+__device__ __forceinline__ bool group_finish_pixel(const Epi& e, long long pix, bool valid, int gl,
+                                                   int G, ZF zf) {
+  const int C = e.C, nch = C >> 3;
+  const int s = valid ? (int)(pix / e.HW) : 0;
+  const bool first = valid && e.first[s] != 0;
+  T* dl = reinterpret_cast<T*>(e.delta) + pix * C;
+  float* O = e.O ? e.O + pix * C : nullptr;
+  bool upd = valid;
+  if (e.act != ACT_NONE) {
+    TC* A = reinterpret_cast<TC*>(e.xA) + pix * C;
+    TC* Tt = reinterpret_cast<TC*>(e.xT) + pix * C;
+    float z[2][8], a[2][8], t[2][8];
+    float mx = 0.f;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = gl + q * G;
+      if (valid && j < nch) {
+        zf(j, z[q]);
+        if (first) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) a[q][k] = t[q][k] = 0.f;
+        } else {
+          ld8(A + 8 * j, a[q]);
+          ld8(Tt + 8 * j, t[q]);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float prev = first ? 0.f : act_f(e.act, a[q][k], e.act_param);
+          const float d = act_f(e.act, a[q][k] + t[q][k] + z[q][k], e.act_param) - prev;   // Eq. 5
+          mx = fmaxf(mx, fabsf(d));
+        }
+      }
+    }
+    for (int o = G >> 1; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float eps = *e.eps;
+    upd = valid && (first || eps < 0.f || mx > eps);         // strict rule (DESIGN Z1)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = gl + q * G;
+      if (valid && j < nch) {
+        if (upd) {
+          float sv[8], dv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            sv[k] = a[q][k] + t[q][k] + z[q][k];
+            const float prev = first ? 0.f : act_f(e.act, a[q][k], e.act_param);
+            dv[k] = rnd<T>(act_f(e.act, sv[k], e.act_param) - prev);
+          }
+          st8(A + 8 * j, sv);                                // Eq. 6
+          st8_zero(Tt + 8 * j);
+          st8(dl + 8 * j, dv);
+          if (O) {
+            float o8[8];
+            if (first) {
+              st8(O + 8 * j, dv);
+            } else {
+              ld8(O + 8 * j, o8);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) o8[k] += dv[k];
+              st8(O + 8 * j, o8);
+            }
+          }
+        } else {
+          float tv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) tv[k] = t[q][k] + z[q][k];
+          st8(Tt + 8 * j, tv);                               // x^T += dx
+        }
+      }
+    }
+  } else if (valid) {
+    for (int j = gl; j < nch; j += G) {
+      float z[8];
+      zf(j, z);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) z[k] = rnd<T>(z[k]);
+      st8(dl + 8 * j, z);
+      if (O) {
+        if (first) {
+          st8(O + 8 * j, z);
+        } else {
+          float o8[8];
+          ld8(O + 8 * j, o8);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) o8[k] += z[k];
+          st8(O + 8 * j, o8);
+        }
+      }
+    }
+  }
+  if (valid && gl == 0) e.mask[pix] = upd ? 1 : 0;
+  return upd;
+}
+
 // Flush a per-warp counter with one atomic (lane 0 holds the count).
 __device__ __forceinline__ void warp_count_flush(unsigned long long* ctr, int lane, unsigned n) {
   if (ctr && lane == 0 && n) atomicAdd(ctr, (unsigned long long)n);
+}
+
+// lanes per pixel for a C-channel op (largest power of two <= min(32, C/8))
+__host__ __device__ __forceinline__ int group_lanes(int C) {
+  int n = C >> 3, g = 1;
+  while (g * 2 <= n && g < 32) g *= 2;
+  return g;
 }
 
 }  // namespace dcnn

@@ -74,7 +74,7 @@ struct Op {
 }  // namespace
 
 struct dcnn_net {
-  int device = 0, S = 1, dtype = 0, esz = 4;
+  int device = 0, S = 1, dtype = 0, esz = 4, cache32 = 0, cesz = 4;
   int inH = 0, inW = 0, inC = 0, radius = 0, flags = 0;
   std::vector<Op> ops;
   std::vector<int> outputs;
@@ -156,6 +156,7 @@ static bool plan_tc(Op& o, int dtype, int flags) {
   const int s = o.stride, d = o.dil;
   p.HH = 15 * s + (o.kh - 1) * d + 1;
   p.WW = 7 * s + (o.kw - 1) * d + 1;
+  if (p.HH * p.WW > 1024) return false;                 // halo mask staging buffer
   const int WQ = (p.WW + s - 1) / s;
   p.WWp = s * WQ;
   const size_t budget = 227 * 1024 - 384;
@@ -264,10 +265,12 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       cp.delta_in = src_delta(o.in[0]); cp.mask_in = src_mask(o.in[0]);
       cp.wt = o.wt; cp.bias = o.bias;
       cp.list = o.list_cc; cp.count = n->counts + o.cnt_idx;
+      cp.vec = (o.C % 8 == 0) ? 1 : 0;
+      cp.G = group_lanes(o.C);
       cp.ep = make_epi(n, i);
       {
         TimeScope ts(n, st, DCNN_KCLASS_CONV);
-        launch_conv_cc(cp, n->dtype, o.grid_cc, st);
+        launch_conv_cc(cp, n->dtype, n->cache32, o.grid_cc, st);
       }
       ++k;
       if (o.tc) {
@@ -278,7 +281,7 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
         p.count = n->counts + o.cnt_idx + 1;
         p.ep = make_epi(n, i);
         TimeScope ts(n, st, DCNN_KCLASS_CONV);
-        launch_conv_tc(p, o.grid_tc, st);
+        launch_conv_tc(p, n->cache32, o.grid_tc, st);
         ++k;
       }
     } else {
@@ -293,15 +296,20 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       }
       pp.k = o.kh; pp.stride = o.stride; pp.pad = o.pad; pp.up = o.up;
       pp.scale = o.scale; pp.shift = o.shift; pp.poolA = o.poolA;
+      bool vec = o.C % 8 == 0;
+      if (o.kind == DCNN_OP_CONCAT)
+        for (int j = 0; j < o.n_in; ++j) vec = vec && o.Cin[j] % 8 == 0;
+      pp.vec = vec ? 1 : 0;
+      pp.G = group_lanes(o.C);
       pp.ep = make_epi(n, i);
       {
         TimeScope ts(n, st, DCNN_KCLASS_POINTWISE);
-        launch_pointwise(pp, n->dtype, st);
+        launch_pointwise(pp, n->dtype, n->cache32, st);
       }
       ++k;
       if (o.kind == DCNN_OP_MAXPOOL) {
         TimeScope ts(n, st, DCNN_KCLASS_POINTWISE);
-        launch_pool_update(pp, n->dtype, st);
+        launch_pool_update(pp, n->dtype, n->cache32, st);
         ++k;
       }
     }
@@ -351,6 +359,8 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   if (d->n_outputs <= 0 || !d->output_ops) return fail(DCNN_ERR_ARG, "no outputs");
   if (d->input_dilation < 0 || d->input_dilation > 16) return fail(DCNN_ERR_UNSUPPORTED, "input_dilation must be in [0,16]");
   n->device = d->device; n->S = d->n_streams; n->dtype = d->dtype; n->esz = d->dtype == DCNN_F16 ? 2 : 4;
+  n->cache32 = (d->dtype == DCNN_F16 && (d->flags & DCNN_FLAG_FP32_CACHES)) ? 1 : 0;
+  n->cesz = n->cache32 ? 4 : n->esz;
   n->inH = d->in_h; n->inW = d->in_w; n->inC = d->in_c; n->radius = d->input_dilation; n->flags = d->flags;
   CUDA_TRY(cudaSetDevice(n->device));
   const int L = d->n_layers;
@@ -478,10 +488,10 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
     if ((r = dalloc(n, &o.delta, px * o.C * es))) return r;
     if ((r = dalloc(n, &o.mask, px))) return r;
     if (o.act != DCNN_ACT_NONE) {
-      if ((r = dalloc(n, &o.xA, px * o.C * es))) return r;
-      if ((r = dalloc(n, &o.xT, px * o.C * es))) return r;
+      if ((r = dalloc(n, &o.xA, px * o.C * n->cesz))) return r;
+      if ((r = dalloc(n, &o.xT, px * o.C * n->cesz))) return r;
     }
-    if (o.kind == DCNN_OP_MAXPOOL && (r = dalloc(n, &o.poolA, S * o.Hi * o.Wi * o.C * es))) return r;
+    if (o.kind == DCNN_OP_MAXPOOL && (r = dalloc(n, &o.poolA, S * o.Hi * o.Wi * o.C * n->cesz))) return r;
     if (o.out_slot >= 0) {
       if ((r = dalloc(n, &o.O, px * o.C * sizeof(float)))) return r;
       CUDA_TRY(cudaMemset(o.O, 0, px * o.C * sizeof(float)));
@@ -715,10 +725,10 @@ dcnn_status dcnn_debug_read(dcnn_net* n, int32_t op, int32_t which, void* host, 
     switch (which) {
       case DCNN_BUF_DELTA: src = o.delta; nb = px * o.C * es; break;
       case DCNN_BUF_MASK: src = o.mask; nb = px; break;
-      case DCNN_BUF_XA: src = o.xA; nb = px * o.C * es; break;
-      case DCNN_BUF_XT: src = o.xT; nb = px * o.C * es; break;
+      case DCNN_BUF_XA: src = o.xA; nb = px * o.C * n->cesz; break;
+      case DCNN_BUF_XT: src = o.xT; nb = px * o.C * n->cesz; break;
       case DCNN_BUF_OUT: src = o.O; nb = px * o.C * 4; break;
-      case DCNN_BUF_POOLA: src = o.poolA; nb = (size_t)n->S * o.Hi * o.Wi * o.C * es; break;
+      case DCNN_BUF_POOLA: src = o.poolA; nb = (size_t)n->S * o.Hi * o.Wi * o.C * n->cesz; break;
       default: return fail(DCNN_ERR_ARG, "which");
     }
     if (!src) return fail(DCNN_ERR_ARG, "buffer not present for this op");

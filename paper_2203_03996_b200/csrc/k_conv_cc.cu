@@ -94,7 +94,7 @@ size_t conv_cc_smem(const ConvCCParams& p) {
   return win + msk + zt;
 }
 
-template <typename T>
+template <typename T, typename TC>
 __global__ void __launch_bounds__(CC_THREADS) k_conv_cc(ConvCCParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   float* win = reinterpret_cast<float*>(smem);
@@ -190,32 +190,55 @@ __global__ void __launch_bounds__(CC_THREADS) k_conv_cc(ConvCCParams p) {
     }
     __syncthreads();
     // (c) fused epilogue: bias on the first frame, activation + truncation, output
-    for (int pl = warp; pl < P; pl += CC_THREADS / 32) {
-      const int oy = oy0 + pl / p.STW, ox = ox0 + pl % p.STW;
-      if (oy >= p.Ho || ox >= p.Wo) continue;
-      const long long pix = ((long long)s * p.Ho + oy) * p.Wo + ox;
-      if (!p.ep.mask[pix]) continue;         // m_conv from a2; skipped pixels stay 0
-      const float* zr = zt + (size_t)pl * p.Cp;
-      const float* bias = p.bias;
-      const bool up = warp_finish_pixel<T>(p.ep, pix, lane, [&](int c) {
-        return first ? zr[c] + bias[c] : zr[c];
-      });
-      nact += up ? 1 : 0;
+    const float* bias = p.bias;
+    if (p.vec) {
+      const int G = p.G, PPW = 32 / G, gi = lane / G, gl = lane % G;
+      for (int b0 = warp * PPW; b0 < P; b0 += (CC_THREADS / 32) * PPW) {
+        const int pl = b0 + gi;
+        const int oy = oy0 + pl / p.STW, ox = ox0 + pl % p.STW;
+        const long long pix = ((long long)s * p.Ho + oy) * p.Wo + ox;
+        const bool valid = pl < P && oy < p.Ho && ox < p.Wo && p.ep.mask[pix];   // m_conv from a2
+        const float* zr = zt + (size_t)pl * p.Cp;
+        const bool up = group_finish_pixel<T, TC>(p.ep, pix, valid, gl, G, [&](int j, float z[8]) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) z[k] = first ? zr[8 * j + k] + bias[8 * j + k] : zr[8 * j + k];
+        });
+        if (valid && gl == 0 && up) ++nact;
+      }
+    } else {
+      for (int pl = warp; pl < P; pl += CC_THREADS / 32) {
+        const int oy = oy0 + pl / p.STW, ox = ox0 + pl % p.STW;
+        if (oy >= p.Ho || ox >= p.Wo) continue;
+        const long long pix = ((long long)s * p.Ho + oy) * p.Wo + ox;
+        if (!p.ep.mask[pix]) continue;         // m_conv from a2; skipped pixels stay 0
+        const float* zr = zt + (size_t)pl * p.Cp;
+        const bool up = warp_finish_pixel<T, TC>(p.ep, pix, lane, [&](int c) {
+          return first ? zr[c] + bias[c] : zr[c];
+        });
+        if (lane == 0 && up) ++nact;
+      }
     }
   }
+  nact = (unsigned)warp_sum((int)nact);
   warp_count_flush(p.ep.n_active, lane, nact);
 }
 
 cudaError_t conv_cc_init() {
-  cudaError_t e = cudaFuncSetAttribute(k_conv_cc<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(k_conv_cc<__half, __half>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_conv_cc<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  e = cudaFuncSetAttribute(k_conv_cc<__half, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_conv_cc<float, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
-void launch_conv_cc(const ConvCCParams& p, int dtype, int grid, cudaStream_t st) {
+void launch_conv_cc(const ConvCCParams& p, int dtype, int cache32, int grid, cudaStream_t st) {
   const size_t smem = conv_cc_smem(p);
-  if (dtype == 1) k_conv_cc<__half><<<grid, CC_THREADS, smem, st>>>(p);
-  else k_conv_cc<float><<<grid, CC_THREADS, smem, st>>>(p);
+  if (dtype == 1) {
+    if (cache32) k_conv_cc<__half, float><<<grid, CC_THREADS, smem, st>>>(p);
+    else k_conv_cc<__half, __half><<<grid, CC_THREADS, smem, st>>>(p);
+  } else {
+    k_conv_cc<float, float><<<grid, CC_THREADS, smem, st>>>(p);
+  }
 }
 
 }  // namespace dcnn

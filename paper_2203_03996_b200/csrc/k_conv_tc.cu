@@ -28,14 +28,17 @@ namespace dcnn {
 constexpr int TC_THREADS = 320;
 
 struct TcSmem {                 // byte offsets inside dynamic shared memory
-  uint32_t bar, tmem_slot, a0, a1, b0;
+  uint32_t bar, tmem_slot, hmask, a0, a1, b0;
 };
+
+constexpr int TC_HMASK_BYTES = 1024;   // halo update mask of the current tile (u8)
 
 __host__ __device__ inline TcSmem tc_layout(const ConvTCParams& p) {
   TcSmem L;
   L.bar = 0;                                  // up to 32 mbarriers
   L.tmem_slot = 32 * 8;
-  L.a0 = 384;
+  L.hmask = 384;
+  L.a0 = 384 + TC_HMASK_BYTES;
   L.a1 = L.a0 + p.a_bytes;
   L.b0 = L.a1 + p.a_bytes;
   return L;
@@ -46,6 +49,7 @@ size_t conv_tc_smem(const ConvTCParams& p) {
   return (size_t)L.b0 + (size_t)p.stages * p.b_bytes;
 }
 
+template <typename TC>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const TcSmem L = tc_layout(p);
@@ -58,6 +62,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
   uint64_t* acc_full = bars + 20;             // [2]
   uint64_t* acc_empty = bars + 22;            // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
+  uint8_t* hmask = smem + L.hmask;
   unsigned char* abuf[2] = {smem + L.a0, smem + L.a1};
   unsigned char* bstage = smem + L.b0;
 
@@ -85,9 +90,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
 
   if (warp >= 4 && warp < 8) {
     // ---------------------------------------------------------------- halo loaders
+    // (a) of PAPER.md:654: active inputs are copied with 16-byte cp.async, inactive or
+    // out-of-image pixels are zero-filled by the copy itself (src-size 0): stale
+    // deltas are never read.  The tile's halo mask is staged once in smem.
     const int lt = tid - 128;
     const int nch = p.BK / 8;
-    const int items = p.HH * p.WW * nch;
+    const int npx = p.HH * p.WW;
+    const int items = npx * nch;
     const int WQ = p.WWp / p.stride;
     int q = 0;                                 // global c-block counter (buffer ring)
     for (int ti = blockIdx.x; ti < count; ti += gridDim.x) {
@@ -96,23 +105,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
       const int ty = (tile / p.ntx) % p.nty, tx = tile % p.ntx;
       const int iy0 = ty * 16 * p.stride - p.pad, ix0 = tx * 8 * p.stride - p.pad;
       const uint8_t* mi = p.mask_in + (long long)s * p.H * p.W;
+      tc::named_bar_sync(1, 128);              // previous tile's mask no longer in use
+      for (int px = lt; px < npx; px += 128) {
+        const int iy = iy0 + px / p.WW, ix = ix0 + px % p.WW;
+        hmask[px] = (iy >= 0 && iy < p.H && ix >= 0 && ix < p.W) ? mi[iy * p.W + ix] : 0;
+      }
+      tc::named_bar_sync(1, 128);
+      const __half* src0 = p.delta_in + (long long)s * p.H * p.W * p.Ci;
       for (int cb = 0; cb < p.ncb; ++cb, ++q) {
         const int b = q & 1;
         tc::mbar_wait(&a_empty[b], ((q >> 1) & 1) ^ 1);
-        unsigned char* A = abuf[b];
+        const uint32_t A = tc::smem_u32(abuf[b]);
         const int c0 = cb * p.BK;
         for (int it = lt; it < items; it += 128) {
           const int px = it / nch, ch = it % nch;
           const int hy = px / p.WW, hx = px % p.WW;
-          const int iy = iy0 + hy, ix = ix0 + hx;
-          uint4 v = make_uint4(0, 0, 0, 0);
-          if (iy >= 0 && iy < p.H && ix >= 0 && ix < p.W && mi[iy * p.W + ix])
-            v = __ldg(reinterpret_cast<const uint4*>(p.delta_in + (((long long)s * p.H + iy) * p.W + ix) * p.Ci +
-                                                      c0 + ch * 8));
+          const bool v = hmask[px] != 0;
+          const __half* g = v ? src0 + ((long long)(iy0 + hy) * p.W + (ix0 + hx)) * p.Ci + c0 + ch * 8 : src0;
           const int pi = hy * p.WWp + (hx % p.stride) * WQ + hx / p.stride;
-          *reinterpret_cast<uint4*>(A + (size_t)ch * p.plane + (size_t)pi * 16) = v;
+          tc::cp_async16(A + (uint32_t)(ch * p.plane + pi * 16), g, v);
         }
-        tc::fence_proxy_async_smem();          // generic-proxy stores -> tensor-core reads
+        tc::cp_async_wait_all();
+        tc::fence_proxy_async_smem();          // generic-proxy writes -> tensor-core reads
         tc::mbar_arrive(&a_full[b]);
       }
     }
@@ -172,6 +186,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 0-3)
+    // thread = TMEM lane = output pixel; Eqs. 4-6 with the per-pixel max-norm
+    // computed in registers (pass 1), then caches / delta / output written (pass 2).
     const Epi& e = p.ep;
     const int C = e.C;
     const bool vec = (C % 8) == 0;
@@ -193,88 +209,95 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
       const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * p.acc_stride);
       __half* dl = reinterpret_cast<__half*>(e.delta) + pix * C;
       float* O = e.O ? e.O + pix * C : nullptr;
+      TC* A = reinterpret_cast<TC*>(e.xA) + pix * C;
+      TC* Tt = reinterpret_cast<TC*>(e.xT) + pix * C;
+      const bool trunc = e.act != ACT_NONE;
       bool upd = act;
-      if (e.act != ACT_NONE) {
-        __half* A = reinterpret_cast<__half*>(e.xA) + pix * C;
-        __half* Tt = reinterpret_cast<__half*>(e.xT) + pix * C;
+      // load 16 channels of z (+bias on the first frame), x^A, x^T
+      auto fetch = [&](int c0, float z[16], float a[16], float t[16]) {
+        uint32_t r[16];
+        tc::tmem_ld16(tbase + c0, r);
+        tc::tmem_wait_ld();
+        if (!act) return;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) z[k] = __uint_as_float(r[k]) + ((first && c0 + k < C) ? p.bias[c0 + k] : 0.f);
+        if (!trunc) return;
+        if (first) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) a[k] = t[k] = 0.f;
+        } else if (vec && c0 + 16 <= C) {
+          ld8(A + c0, a); ld8(A + c0 + 8, a + 8);
+          ld8(Tt + c0, t); ld8(Tt + c0 + 8, t + 8);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            a[k] = c0 + k < C ? ld(A + c0 + k) : 0.f;
+            t[k] = c0 + k < C ? ld(Tt + c0 + k) : 0.f;
+          }
+        }
+      };
+      if (trunc) {
         float mx = 0.f;
         for (int c0 = 0; c0 < C; c0 += 16) {
-          uint32_t r[16];
-          tc::tmem_ld16(tbase + c0, r);
-          tc::tmem_wait_ld();
+          float z[16], a[16], t[16];
+          fetch(c0, z, a, t);
           if (act) {
-            float a[16], t[16];
-            if (vec && c0 + 16 <= C && !first) {
-              const uint4* pa = reinterpret_cast<const uint4*>(A + c0);
-              const uint4* pt = reinterpret_cast<const uint4*>(Tt + c0);
-              uint4 va[2] = {pa[0], pa[1]}, vt[2] = {pt[0], pt[1]};
-              const __half* ha = reinterpret_cast<const __half*>(va);
-              const __half* ht = reinterpret_cast<const __half*>(vt);
 #pragma unroll
-              for (int k = 0; k < 16; ++k) { a[k] = __half2float(ha[k]); t[k] = __half2float(ht[k]); }
-            } else {
-#pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                const int c = c0 + k;
-                a[k] = (first || c >= C) ? 0.f : __half2float(A[c]);
-                t[k] = (first || c >= C) ? 0.f : __half2float(Tt[c]);
-              }
-            }
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const int c = c0 + k;
-              if (c < C) {
-                const float z = __uint_as_float(r[k]) + (first ? p.bias[c] : 0.f);
-                const float sum = a[k] + t[k] + z;
+            for (int k = 0; k < 16; ++k)
+              if (c0 + k < C) {
                 const float prev = first ? 0.f : act_f(e.act, a[k], e.act_param);
-                mx = fmaxf(mx, fabsf(act_f(e.act, sum, e.act_param) - prev));
+                mx = fmaxf(mx, fabsf(act_f(e.act, a[k] + t[k] + z[k], e.act_param) - prev));
               }
-            }
           }
         }
         upd = act && (first || eps < 0.f || mx > eps);
-        for (int c0 = 0; c0 < C; c0 += 16) {
-          uint32_t r[16];
-          tc::tmem_ld16(tbase + c0, r);
-          tc::tmem_wait_ld();
-          if (act) {
+      }
+      for (int c0 = 0; c0 < C; c0 += 16) {
+        float z[16], a[16], t[16];
+        fetch(c0, z, a, t);
+        if (!act) continue;
+        float o[16];          // values to store: delta (upd / linear) or new x^T
+        float sv[16];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const int c = c0 + k;
-              if (c < C) {
-                const float z = __uint_as_float(r[k]) + (first ? p.bias[c] : 0.f);
-                const float a = first ? 0.f : __half2float(A[c]);
-                const float t = first ? 0.f : __half2float(Tt[c]);
-                if (upd) {
-                  const float sum = a + t + z;
-                  const float prev = first ? 0.f : act_f(e.act, a, e.act_param);
-                  const __half dq = __float2half_rn(act_f(e.act, sum, e.act_param) - prev);
-                  A[c] = __float2half_rn(sum);               // Eq. 6
-                  Tt[c] = __float2half_rn(0.f);
-                  dl[c] = dq;
-                  if (O) O[c] = first ? __half2float(dq) : O[c] + __half2float(dq);
-                } else {
-                  Tt[c] = __float2half_rn(t + z);            // x^T += dx
-                }
-              }
-            }
+        for (int k = 0; k < 16; ++k) {
+          if (!trunc) {
+            o[k] = __half2float(__float2half_rn(z[k]));
+          } else if (upd) {
+            sv[k] = a[k] + t[k] + z[k];                                       // Eq. 6
+            const float prev = first ? 0.f : act_f(e.act, a[k], e.act_param);
+            o[k] = __half2float(__float2half_rn(act_f(e.act, sv[k], e.act_param) - prev));
+          } else {
+            o[k] = t[k] + z[k];                                               // x^T += dx
           }
         }
-      } else {
-        for (int c0 = 0; c0 < C; c0 += 16) {
-          uint32_t r[16];
-          tc::tmem_ld16(tbase + c0, r);
-          tc::tmem_wait_ld();
-          if (act) {
+        const bool full = vec && c0 + 16 <= C;
+        if (trunc && !upd) {
+          if (full) { st8(Tt + c0, o); st8(Tt + c0 + 8, o + 8); }
+          else for (int k = 0; k < 16 && c0 + k < C; ++k) st(Tt + c0 + k, o[k]);
+          continue;
+        }
+        if (full) {
+          st8(dl + c0, o); st8(dl + c0 + 8, o + 8);
+          if (trunc) {
+            st8(A + c0, sv); st8(A + c0 + 8, sv + 8);
+            st8_zero(Tt + c0); st8_zero(Tt + c0 + 8);
+          }
+          if (O) {
+            float ov[16];
+            if (first) {
+              st8(O + c0, o); st8(O + c0 + 8, o + 8);
+            } else {
+              ld8(O + c0, ov); ld8(O + c0 + 8, ov + 8);
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const int c = c0 + k;
-              if (c < C) {
-                const __half zq = __float2half_rn(__uint_as_float(r[k]) + (first ? p.bias[c] : 0.f));
-                dl[c] = zq;
-                if (O) O[c] = first ? __half2float(zq) : O[c] + __half2float(zq);
-              }
+              for (int k = 0; k < 16; ++k) ov[k] += o[k];
+              st8(O + c0, ov); st8(O + c0 + 8, ov + 8);
             }
+          }
+        } else {
+          for (int k = 0; k < 16 && c0 + k < C; ++k) {
+            st(dl + c0 + k, o[k]);
+            if (trunc) { st(A + c0 + k, sv[k]); st(Tt + c0 + k, 0.f); }
+            if (O) O[c0 + k] = first ? o[k] : O[c0 + k] + o[k];
           }
         }
       }
@@ -295,11 +318,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
 }
 
 cudaError_t conv_tc_init() {
-  return cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(k_conv_tc<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_conv_tc<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
-void launch_conv_tc(const ConvTCParams& p, int grid, cudaStream_t st) {
-  k_conv_tc<<<grid, TC_THREADS, conv_tc_smem(p), st>>>(p);
+void launch_conv_tc(const ConvTCParams& p, int cache32, int grid, cudaStream_t st) {
+  if (cache32) k_conv_tc<float><<<grid, TC_THREADS, conv_tc_smem(p), st>>>(p);
+  else k_conv_tc<__half><<<grid, TC_THREADS, conv_tc_smem(p), st>>>(p);
 }
 
 }  // namespace dcnn

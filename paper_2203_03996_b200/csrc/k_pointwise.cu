@@ -1,6 +1,6 @@
 // k_pointwise.cu -- a5 (standalone activation + truncation), a6 (add, concat,
 // nearest upsample, affine), a7 (max-pool, avg-pool) and a8 (output accumulation,
-// fused into every op's epilogue through warp_finish_pixel).
+// fused into every op's epilogue).
 //
 // PAPER.md:309 (§3.4) "sparse implementations for most common layers ...
 // pooling layers, upsampling layers, activations, concatenations and additions";
@@ -8,9 +8,10 @@
 //
 // Work distribution: each warp owns 32 consecutive output pixels.  Lane i
 // computes the output mask of pixel i (coalesced u8 reads), the warp ballots,
-// writes 0 masks for inactive pixels and then finishes every active pixel
-// cooperatively (lanes stride channels, so NHWC rows are read coalesced).
-// Inactive pixels cost one mask byte; their deltas are never touched
+// writes 0 masks for inactive pixels, then finishes the active pixels 32/G at a
+// time: a group of G lanes per pixel, each lane moving 16-byte (fp16) / 32-byte
+// (fp32) channel chunks, so every NHWC row is read and written with full
+// sectors.  Inactive pixels cost one mask byte; their deltas are never touched
 // ("we do not need to initialize unprocessed values").
 #include "kernels.h"
 
@@ -19,18 +20,18 @@ namespace dcnn {
 enum Kind { K_CONV = 0, K_ACT = 1, K_MAXPOOL = 2, K_AVGPOOL = 3, K_UP = 4, K_ADD = 5, K_CONCAT = 6,
             K_AFFINE = 7 };
 
-template <typename T>
+template <int KIND>
 __device__ __forceinline__ bool pw_mask(const PwParams& p, long long pix, int s, bool first) {
   if (first) return true;
-  if (p.kind == K_ACT || p.kind == K_AFFINE) return p.min[0][pix] != 0;
-  if (p.kind == K_ADD || p.kind == K_CONCAT) {
+  if (KIND == K_ACT || KIND == K_AFFINE) return p.min[0][pix] != 0;
+  if (KIND == K_ADD || KIND == K_CONCAT) {
     bool m = false;
     for (int k = 0; k < p.n_in; ++k) m |= p.min[k][pix] != 0;
     return m;
   }
   const long long HWo = (long long)p.H * p.W;
   const int y = (int)((pix % HWo) / p.W), x = (int)(pix % p.W);
-  if (p.kind == K_UP) return p.min[0][((long long)s * p.Hi + y / p.up) * p.Wi + x / p.up] != 0;
+  if (KIND == K_UP) return p.min[0][((long long)s * p.Hi + y / p.up) * p.Wi + x / p.up] != 0;
   // pools: window OR (padding inactive)
   const uint8_t* mi = p.min[0] + (long long)s * p.Hi * p.Wi;
   for (int ky = 0; ky < p.k; ++ky) {
@@ -44,152 +45,239 @@ __device__ __forceinline__ bool pw_mask(const PwParams& p, long long pix, int s,
   return false;
 }
 
-template <typename T>
-__device__ __forceinline__ bool pw_finish(const PwParams& p, long long pix, int s, bool first,
-                                          int lane) {
+// pre-activation delta of 8 channels [8j, 8j+8) of output pixel pix
+template <typename T, typename TC, int KIND>
+__device__ __forceinline__ void pw_chunk(const PwParams& p, long long pix, int s, bool first,
+                                         const bool (&mk)[4], int j, float z[8]) {
   const int C = p.ep.C;
   const T* in0 = reinterpret_cast<const T*>(p.in[0]);
-  switch (p.kind) {
-    case K_ACT:
-      return warp_finish_pixel<T>(p.ep, pix, lane, [&](int c) { return ld(in0 + pix * C + c); });
-    case K_AFFINE:
-      return warp_finish_pixel<T>(p.ep, pix, lane, [&](int c) {
-        return ld(in0 + pix * C + c) * p.scale[c] + (first ? p.shift[c] : 0.f);
-      });
-    case K_ADD: {
-      bool mk[4];
-      for (int k = 0; k < 4; ++k) mk[k] = k < p.n_in && (first || p.min[k][pix] != 0);
-      return warp_finish_pixel<T>(p.ep, pix, lane, [&](int c) {
-        float z = 0.f;
-        for (int k = 0; k < p.n_in; ++k)
-          if (mk[k]) z += ld(reinterpret_cast<const T*>(p.in[k]) + pix * C + c);   // Z10
-        return z;
-      });
+  if (KIND == K_ACT) {
+    ld8(in0 + pix * C + 8 * j, z);
+  } else if (KIND == K_AFFINE) {
+    ld8(in0 + pix * C + 8 * j, z);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) z[k] = z[k] * p.scale[8 * j + k] + (first ? p.shift[8 * j + k] : 0.f);
+  } else if (KIND == K_ADD) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) z[k] = 0.f;
+    for (int i = 0; i < p.n_in; ++i)
+      if (mk[i]) {                                          // Z10: absent operand = 0
+        float v[8];
+        ld8(reinterpret_cast<const T*>(p.in[i]) + pix * C + 8 * j, v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) z[k] += v[k];
+      }
+  } else if (KIND == K_CONCAT) {
+    int i = 0, off = 0;
+    while (8 * j >= off + p.Cin[i]) { off += p.Cin[i]; ++i; }
+    if (mk[i]) {
+      ld8(reinterpret_cast<const T*>(p.in[i]) + pix * p.Cin[i] + (8 * j - off), z);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) z[k] = 0.f;              // zero-filled channels (Z10)
     }
-    case K_CONCAT: {
-      bool mk[4];
-      for (int k = 0; k < 4; ++k) mk[k] = k < p.n_in && (first || p.min[k][pix] != 0);
-      return warp_finish_pixel<T>(p.ep, pix, lane, [&](int c) {
-        int k = 0, off = 0;
-        while (c >= off + p.Cin[k]) { off += p.Cin[k]; ++k; }
-        return mk[k] ? ld(reinterpret_cast<const T*>(p.in[k]) + pix * p.Cin[k] + (c - off)) : 0.f;
-      });
-    }
-    case K_UP: {
-      const long long HWo = (long long)p.H * p.W;
-      const int y = (int)((pix % HWo) / p.W), x = (int)(pix % p.W);
-      const long long src = ((long long)s * p.Hi + y / p.up) * p.Wi + x / p.up;
-      return warp_finish_pixel<T>(p.ep, pix, lane, [&](int c) { return ld(in0 + src * C + c); });
-    }
-    default: {  // pools
-      const long long HWo = (long long)p.H * p.W;
-      const int y = (int)((pix % HWo) / p.W), x = (int)(pix % p.W);
-      const uint8_t* mi = p.min[0] + (long long)s * p.Hi * p.Wi;
-      const T* A = reinterpret_cast<const T*>(p.poolA);
-      const long long base = (long long)s * p.Hi * p.Wi;
-      const bool isMax = p.kind == K_MAXPOOL;
-      const float inv = 1.f / (float)(p.k * p.k);
-      return warp_finish_pixel<T>(p.ep, pix, lane, [&](int c) {
-        float mnew = -INFINITY, mold = -INFINITY, sum = 0.f;
-        for (int ky = 0; ky < p.k; ++ky) {
-          const int iy = y * p.stride - p.pad + ky;
-          if (iy < 0 || iy >= p.Hi) continue;
-          for (int kx = 0; kx < p.k; ++kx) {
-            const int ix = x * p.stride - p.pad + kx;
-            if (ix < 0 || ix >= p.Wi) continue;
-            const long long q = base + (long long)iy * p.Wi + ix;
-            const bool act = first || mi[iy * p.Wi + ix];
-            const float d = act ? ld(in0 + q * C + c) : 0.f;
-            if (isMax) {
-              const float a = first ? 0.f : ld(A + q * C + c);
-              mnew = fmaxf(mnew, a + d);                       // max_w(x^A + dx)
-              mold = fmaxf(mold, a);                           // max_w(x^A)
-            } else {
-              sum += d;
-            }
-          }
+  } else if (KIND == K_UP) {
+    const long long HWo = (long long)p.H * p.W;
+    const int y = (int)((pix % HWo) / p.W), x = (int)(pix % p.W);
+    const long long src = ((long long)s * p.Hi + y / p.up) * p.Wi + x / p.up;
+    ld8(in0 + src * C + 8 * j, z);
+  } else {  // pools
+    const long long HWo = (long long)p.H * p.W;
+    const int y = (int)((pix % HWo) / p.W), x = (int)(pix % p.W);
+    const uint8_t* mi = p.min[0] + (long long)s * p.Hi * p.Wi;
+    const TC* A = reinterpret_cast<const TC*>(p.poolA);
+    const long long base = (long long)s * p.Hi * p.Wi;
+    float mnew[8], mold[8], sum[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { mnew[k] = -INFINITY; mold[k] = -INFINITY; sum[k] = 0.f; }
+    for (int ky = 0; ky < p.k; ++ky) {
+      const int iy = y * p.stride - p.pad + ky;
+      if (iy < 0 || iy >= p.Hi) continue;
+      for (int kx = 0; kx < p.k; ++kx) {
+        const int ix = x * p.stride - p.pad + kx;
+        if (ix < 0 || ix >= p.Wi) continue;
+        const long long q = base + (long long)iy * p.Wi + ix;
+        const bool act = first || mi[iy * p.Wi + ix];
+        float d[8];
+        if (act) ld8(in0 + q * C + 8 * j, d);
+        else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) d[k] = 0.f;
         }
-        if (isMax) return first ? mnew : mnew - mold;          // Eq. 3
-        return sum * inv;
-      });
+        if (KIND == K_MAXPOOL) {
+          float a[8];
+          if (first) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) a[k] = 0.f;
+          } else {
+            ld8(A + q * C + 8 * j, a);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            mnew[k] = fmaxf(mnew[k], a[k] + d[k]);          // max_w(x^A + dx)
+            mold[k] = fmaxf(mold[k], a[k]);                 // max_w(x^A)
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) sum[k] += d[k];
+        }
+      }
     }
+    const float inv = 1.f / (float)(p.k * p.k);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      z[k] = KIND == K_MAXPOOL ? (first ? mnew[k] : mnew[k] - mold[k]) : sum[k] * inv;   // Eq. 3
   }
 }
 
-template <typename T>
+// scalar channel access (C not a multiple of 8): one warp per active pixel
+template <typename T, typename TC, int KIND>
+__device__ __forceinline__ float pw_scalar(const PwParams& p, long long pix, int s, bool first,
+                                           const bool (&mk)[4], int c) {
+  const int C = p.ep.C;
+  const T* in0 = reinterpret_cast<const T*>(p.in[0]);
+  if (KIND == K_ACT) return ld(in0 + pix * C + c);
+  if (KIND == K_AFFINE) return ld(in0 + pix * C + c) * p.scale[c] + (first ? p.shift[c] : 0.f);
+  if (KIND == K_ADD) {
+    float z = 0.f;
+    for (int i = 0; i < p.n_in; ++i)
+      if (mk[i]) z += ld(reinterpret_cast<const T*>(p.in[i]) + pix * C + c);
+    return z;
+  }
+  if (KIND == K_CONCAT) {
+    int i = 0, off = 0;
+    while (c >= off + p.Cin[i]) { off += p.Cin[i]; ++i; }
+    return mk[i] ? ld(reinterpret_cast<const T*>(p.in[i]) + pix * p.Cin[i] + (c - off)) : 0.f;
+  }
+  const long long HWo = (long long)p.H * p.W;
+  const int y = (int)((pix % HWo) / p.W), x = (int)(pix % p.W);
+  if (KIND == K_UP) {
+    const long long src = ((long long)s * p.Hi + y / p.up) * p.Wi + x / p.up;
+    return ld(in0 + src * C + c);
+  }
+  const uint8_t* mi = p.min[0] + (long long)s * p.Hi * p.Wi;
+  const TC* A = reinterpret_cast<const TC*>(p.poolA);
+  const long long base = (long long)s * p.Hi * p.Wi;
+  float mnew = -INFINITY, mold = -INFINITY, sum = 0.f;
+  for (int ky = 0; ky < p.k; ++ky) {
+    const int iy = y * p.stride - p.pad + ky;
+    if (iy < 0 || iy >= p.Hi) continue;
+    for (int kx = 0; kx < p.k; ++kx) {
+      const int ix = x * p.stride - p.pad + kx;
+      if (ix < 0 || ix >= p.Wi) continue;
+      const long long q = base + (long long)iy * p.Wi + ix;
+      const float d = (first || mi[iy * p.Wi + ix]) ? ld(in0 + q * C + c) : 0.f;
+      if (KIND == K_MAXPOOL) {
+        const float a = first ? 0.f : ld(A + q * C + c);
+        mnew = fmaxf(mnew, a + d);
+        mold = fmaxf(mold, a);
+      } else {
+        sum += d;
+      }
+    }
+  }
+  if (KIND == K_MAXPOOL) return first ? mnew : mnew - mold;
+  return sum / (float)(p.k * p.k);
+}
+
+template <typename T, typename TC, int KIND>
 __global__ void __launch_bounds__(256) k_pointwise(PwParams p) {
   const int lane = threadIdx.x & 31;
   const long long npix = (long long)p.S * p.H * p.W;
   const long long HWo = (long long)p.H * p.W;
   const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int G = p.vec ? p.G : 32;
+  const int PPW = 32 / G, gi = lane / G, gl = lane % G;
   unsigned nact = 0;
   for (long long base = gw * 32; base < npix; base += nw * 32) {
     const long long pix = base + lane;
     bool m = false;
     if (pix < npix) {
       const int s = (int)(pix / HWo);
-      m = pw_mask<T>(p, pix, s, p.ep.first[s] != 0);
+      m = pw_mask<KIND>(p, pix, s, p.ep.first[s] != 0);
       if (!m) p.ep.mask[pix] = 0;
     }
-    unsigned bal = __ballot_sync(0xffffffffu, m);
-    while (bal) {
-      const int j = __ffs(bal) - 1;
-      bal &= bal - 1;
-      const long long q = base + j;
-      const int s = (int)(q / HWo);
-      nact += pw_finish<T>(p, q, s, p.ep.first[s] != 0, lane) ? 1 : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, m);
+    const int n = __popc(bal);
+    for (int r = 0; r < n; r += PPW) {
+      const int k = r + gi;
+      const bool valid = k < n;
+      const long long q = base + (valid ? (int)__fns(bal, 0, k + 1) : 0);
+      const int s = valid ? (int)(q / HWo) : 0;
+      const bool first = valid && p.ep.first[s] != 0;
+      bool mk[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) mk[i] = valid && i < p.n_in && (first || p.min[i][q] != 0);
+      bool up;
+      if (p.vec) {
+        up = group_finish_pixel<T, TC>(p.ep, q, valid, gl, G,
+                                       [&](int j, float z[8]) { pw_chunk<T, TC, KIND>(p, q, s, first, mk, j, z); });
+      } else {
+        up = warp_finish_pixel<T, TC>(p.ep, q, lane,
+                                      [&](int c) { return pw_scalar<T, TC, KIND>(p, q, s, first, mk, c); });
+      }
+      if (valid && gl == 0 && up) ++nact;
     }
   }
-  warp_count_flush(p.ep.n_active, lane, nact);
+  const unsigned tot = (unsigned)warp_sum((int)nact);
+  warp_count_flush(p.ep.n_active, lane, tot);
 }
 
 // max-pool accumulated input update, after the pool outputs were computed from
 // the old values: x^A := x^A + dx on active input pixels (first frame: := dx).
-template <typename T>
+// One thread per (pixel, channel) element; coalesced over channels.
+template <typename T, typename TC>
 __global__ void __launch_bounds__(256) k_pool_update(PwParams p) {
-  const int lane = threadIdx.x & 31;
   const int C = p.ep.C;
-  const long long npix = (long long)p.S * p.Hi * p.Wi;
   const long long HWi = (long long)p.Hi * p.Wi;
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long n = (long long)p.S * HWi * C;
   const T* d = reinterpret_cast<const T*>(p.in[0]);
-  T* A = reinterpret_cast<T*>(p.poolA);
-  for (long long base = gw * 32; base < npix; base += nw * 32) {
-    const long long pix = base + lane;
-    bool m = false;
-    if (pix < npix) m = p.ep.first[pix / HWi] != 0 || p.min[0][pix] != 0;
-    unsigned bal = __ballot_sync(0xffffffffu, m);
-    while (bal) {
-      const int j = __ffs(bal) - 1;
-      bal &= bal - 1;
-      const long long q = base + j;
-      const bool first = p.ep.first[q / HWi] != 0;
-      for (int c = lane; c < C; c += 32) {
-        const float a = first ? 0.f : ld(A + q * C + c);
-        st(A + q * C + c, a + ld(d + q * C + c));
-      }
-    }
+  TC* A = reinterpret_cast<TC*>(p.poolA);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long pix = i / C;
+    const bool first = p.ep.first[pix / HWi] != 0;
+    if (first || p.min[0][pix]) st(A + i, (first ? 0.f : ld(A + i)) + ld(d + i));
   }
 }
 
-static int pw_grid(long long npix) {
-  long long warps = (npix + 31) / 32;
-  long long blocks = (warps + 7) / 8;
-  return (int)(blocks < 148 * 8 ? (blocks < 1 ? 1 : blocks) : 148 * 8);
+static int pw_grid(long long items, int per_block) {
+  long long blocks = (items + per_block - 1) / per_block;
+  return (int)(blocks < 1 ? 1 : (blocks < 148 * 16 ? blocks : 148 * 16));
 }
 
-void launch_pointwise(const PwParams& p, int dtype, cudaStream_t st) {
-  const int grid = pw_grid((long long)p.S * p.H * p.W);
-  if (dtype == 1) k_pointwise<__half><<<grid, 256, 0, st>>>(p);
-  else k_pointwise<float><<<grid, 256, 0, st>>>(p);
+template <typename T, typename TC>
+static void pw_dispatch(const PwParams& p, cudaStream_t st) {
+  const int grid = pw_grid((long long)p.S * p.H * p.W, 256);
+  switch (p.kind) {
+    case K_ACT: k_pointwise<T, TC, K_ACT><<<grid, 256, 0, st>>>(p); break;
+    case K_MAXPOOL: k_pointwise<T, TC, K_MAXPOOL><<<grid, 256, 0, st>>>(p); break;
+    case K_AVGPOOL: k_pointwise<T, TC, K_AVGPOOL><<<grid, 256, 0, st>>>(p); break;
+    case K_UP: k_pointwise<T, TC, K_UP><<<grid, 256, 0, st>>>(p); break;
+    case K_ADD: k_pointwise<T, TC, K_ADD><<<grid, 256, 0, st>>>(p); break;
+    case K_CONCAT: k_pointwise<T, TC, K_CONCAT><<<grid, 256, 0, st>>>(p); break;
+    case K_AFFINE: k_pointwise<T, TC, K_AFFINE><<<grid, 256, 0, st>>>(p); break;
+  }
 }
 
-void launch_pool_update(const PwParams& p, int dtype, cudaStream_t st) {
-  const int grid = pw_grid((long long)p.S * p.Hi * p.Wi);
-  if (dtype == 1) k_pool_update<__half><<<grid, 256, 0, st>>>(p);
-  else k_pool_update<float><<<grid, 256, 0, st>>>(p);
+void launch_pointwise(const PwParams& p, int dtype, int cache32, cudaStream_t st) {
+  if (dtype == 1) {
+    if (cache32) pw_dispatch<__half, float>(p, st);
+    else pw_dispatch<__half, __half>(p, st);
+  } else {
+    pw_dispatch<float, float>(p, st);
+  }
+}
+
+void launch_pool_update(const PwParams& p, int dtype, int cache32, cudaStream_t st) {
+  const int grid = pw_grid((long long)p.S * p.Hi * p.Wi * p.ep.C, 256 * 4);
+  if (dtype == 1) {
+    if (cache32) k_pool_update<__half, float><<<grid, 256, 0, st>>>(p);
+    else k_pool_update<__half, __half><<<grid, 256, 0, st>>>(p);
+  } else {
+    k_pool_update<float, float><<<grid, 256, 0, st>>>(p);
+  }
 }
 
 }  // namespace dcnn

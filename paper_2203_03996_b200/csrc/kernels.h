@@ -55,9 +55,10 @@ struct ConvCCParams {
   const float* wt;              // [kh*kw][Ci][Cp] fp32 (groups expanded densely)
   const float* bias;            // [Co] fp32
   const int* list; const int* count;
+  int vec, G;                   // epilogue: 8-channel chunks (C % 8 == 0), lanes per pixel
   Epi ep;                       // ep.mask holds m_conv on entry for the tile's pixels
 };
-void launch_conv_cc(const ConvCCParams& p, int dtype, int grid, cudaStream_t st);
+void launch_conv_cc(const ConvCCParams& p, int dtype, int cache32, int grid, cudaStream_t st);
 size_t conv_cc_smem(const ConvCCParams& p);
 cudaError_t conv_cc_init();     // once per process/device: raise the dynamic smem limit
 
@@ -82,7 +83,7 @@ struct ConvTCParams {
 };
 size_t conv_tc_smem(const ConvTCParams& p);
 cudaError_t conv_tc_init();
-void launch_conv_tc(const ConvTCParams& p, int grid, cudaStream_t st);
+void launch_conv_tc(const ConvTCParams& p, int cache32, int grid, cudaStream_t st);
 
 // ---------------------------------------------------------------- a6/a7 pointwise ops
 struct PwParams {
@@ -95,12 +96,12 @@ struct PwParams {
   int Cin[4];                   // channels of each input
   int k, stride, pad, up;       // pool window / upsample factor
   const float* scale; const float* shift;  // affine
-  void* poolA;                  // maxpool accumulated input [S,Hi,Wi,C] T
+  void* poolA;                  // maxpool accumulated input [S,Hi,Wi,C] (cache type)
+  int vec, G;                   // 8-channel chunk path, lanes per pixel
   Epi ep;
-  unsigned long long* n_in_active;
 };
-void launch_pointwise(const PwParams& p, int dtype, cudaStream_t st);
-void launch_pool_update(const PwParams& p, int dtype, cudaStream_t st);
+void launch_pointwise(const PwParams& p, int dtype, int cache32, cudaStream_t st);
+void launch_pool_update(const PwParams& p, int dtype, int cache32, cudaStream_t st);
 
 // ---------------------------------------------------------------- control
 void launch_end_frame(uint8_t* first, long long* frame_idx, int S, cudaStream_t st);

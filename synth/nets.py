@@ -59,7 +59,8 @@ class Net:
     outputs: List[int]
     input_eps: float = 0.0
     input_dilation: int = 0
-    dtype: str = "f32"        # storage / compute dtype of deltas, caches, weights
+    dtype: str = "f32"        # storage dtype of frames, deltas, weights (and caches by default)
+    cache_dtype: Optional[str] = None   # storage dtype of x^A, x^T, pool accumulators (None = dtype)
 
     def set_inner_eps(self, eps: float):
         for L in self.layers:
