@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace dcnn {
 
 enum Act { ACT_NONE = 0, ACT_RELU = 1, ACT_SILU = 2, ACT_RELU6 = 3, ACT_LEAKY = 4, ACT_SIGMOID = 5 };
@@ -62,11 +64,38 @@ __device__ __forceinline__ void st8_zero(float* p) {
 __device__ __forceinline__ float act_f(int act, float x, float param) {
   switch (act) {
     case ACT_RELU: return fmaxf(x, 0.f);
-    case ACT_SILU: return x / (1.f + expf(-x));
+    case ACT_SILU: return __fdiv_rn(x, 1.f + expf(-x));
     case ACT_RELU6: return fminf(fmaxf(x, 0.f), 6.f);
-    case ACT_LEAKY: return x > 0.f ? x : param * x;
-    case ACT_SIGMOID: return 1.f / (1.f + expf(-x));
+    case ACT_LEAKY: return x > 0.f ? x : __fmul_rn(param, x);
+    case ACT_SIGMOID: return __fdiv_rn(1.f, 1.f + expf(-x));
     default: return x;
+  }
+}
+
+// compile-time activation (keeps the unrolled epilogues small: one f per kernel).
+// The final products use __fmul_rn so that f(x) is always a rounded value: a
+// contracted FMA in "f(s) - f(a)" would otherwise leave the rounding residual of
+// f(a) when s == a, i.e. a non-zero delta for an unchanged pixel (breaks Z1 at eps 0).
+template <int ACT>
+__device__ __forceinline__ float act_t(float x, float param) {
+  if constexpr (ACT == ACT_RELU) return fmaxf(x, 0.f);
+  else if constexpr (ACT == ACT_SILU) return __fmul_rn(x, __fdividef(1.f, 1.f + __expf(-x)));
+  else if constexpr (ACT == ACT_RELU6) return fminf(fmaxf(x, 0.f), 6.f);
+  else if constexpr (ACT == ACT_LEAKY) return x > 0.f ? x : __fmul_rn(param, x);
+  else if constexpr (ACT == ACT_SIGMOID) return __fdividef(1.f, 1.f + __expf(-x));
+  else return x;
+}
+
+// host-side: call f(std::integral_constant<int, ACT>) for the runtime activation code
+template <typename F>
+inline void act_dispatch(int act, F&& f) {
+  switch (act) {
+    case ACT_RELU: f(std::integral_constant<int, ACT_RELU>{}); break;
+    case ACT_SILU: f(std::integral_constant<int, ACT_SILU>{}); break;
+    case ACT_RELU6: f(std::integral_constant<int, ACT_RELU6>{}); break;
+    case ACT_LEAKY: f(std::integral_constant<int, ACT_LEAKY>{}); break;
+    case ACT_SIGMOID: f(std::integral_constant<int, ACT_SIGMOID>{}); break;
+    default: f(std::integral_constant<int, ACT_NONE>{}); break;
   }
 }
 
@@ -105,7 +134,7 @@ constexpr int MAXK = 16;       // channels per lane in a warp epilogue: C <= 512
 // §3.1 "Truncating small updates" (Eqs. 4-6) when e.act != NONE, else emits z.
 // Scalar channel access (any C); used when C is not a multiple of 8.
 // Returns the pixel's output mask bit (warp-uniform).
-template <typename T, typename TC, typename ZF>
+template <typename T, typename TC, int ACT, typename ZF>
 __device__ __forceinline__ bool warp_finish_pixel(const Epi& e, long long pix, int lane, ZF zf) {
   const int C = e.C;
   const int s = (int)(pix / e.HW);
@@ -113,7 +142,7 @@ __device__ __forceinline__ bool warp_finish_pixel(const Epi& e, long long pix, i
   T* dl = reinterpret_cast<T*>(e.delta) + pix * C;
   float* O = e.O ? e.O + pix * C : nullptr;
   bool upd = true;
-  if (e.act != ACT_NONE) {
+  if constexpr (ACT != ACT_NONE) {
     TC* A = reinterpret_cast<TC*>(e.xA) + pix * C;
     TC* Tt = reinterpret_cast<TC*>(e.xT) + pix * C;
     float zv[MAXK], tv[MAXK], sv[MAXK], dv[MAXK];
@@ -126,8 +155,8 @@ __device__ __forceinline__ bool warp_finish_pixel(const Epi& e, long long pix, i
         const float a = first ? 0.f : ld(A + c);
         const float t = first ? 0.f : ld(Tt + c);
         const float sum = a + t + z;                         // x^A + x^T + dx
-        const float prev = first ? 0.f : act_f(e.act, a, e.act_param);
-        const float d = act_f(e.act, sum, e.act_param) - prev;   // Eq. 5
+        const float prev = first ? 0.f : act_t<ACT>(a, e.act_param);
+        const float d = act_t<ACT>(sum, e.act_param) - prev;   // Eq. 5
         zv[k] = z; tv[k] = t; sv[k] = sum; dv[k] = d;
         mx = fmaxf(mx, fabsf(d));
       }
@@ -166,7 +195,7 @@ __device__ __forceinline__ bool warp_finish_pixel(const Epi& e, long long pix, i
 // truncating, so at most 2 chunks per lane when G = min(32, pow2 <= C/8)).
 // zf(j, z[8]) produces the pre-activation delta of chunk j.  All lanes of the
 // warp must call this together (shuffle reduction).
-template <typename T, typename TC, typename ZF>
+template <typename T, typename TC, int ACT, typename ZF>
 __device__ __forceinline__ bool group_finish_pixel(const Epi& e, long long pix, bool valid, int gl,
                                                    int G, ZF zf) {
   const int C = e.C, nch = C >> 3;
@@ -175,7 +204,7 @@ __device__ __forceinline__ bool group_finish_pixel(const Epi& e, long long pix, 
   T* dl = reinterpret_cast<T*>(e.delta) + pix * C;
   float* O = e.O ? e.O + pix * C : nullptr;
   bool upd = valid;
-  if (e.act != ACT_NONE) {
+  if constexpr (ACT != ACT_NONE) {
     TC* A = reinterpret_cast<TC*>(e.xA) + pix * C;
     TC* Tt = reinterpret_cast<TC*>(e.xT) + pix * C;
     float z[2][8], a[2][8], t[2][8];
@@ -194,8 +223,8 @@ __device__ __forceinline__ bool group_finish_pixel(const Epi& e, long long pix, 
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const float prev = first ? 0.f : act_f(e.act, a[q][k], e.act_param);
-          const float d = act_f(e.act, a[q][k] + t[q][k] + z[q][k], e.act_param) - prev;   // Eq. 5
+          const float prev = first ? 0.f : act_t<ACT>(a[q][k], e.act_param);
+          const float d = act_t<ACT>(a[q][k] + t[q][k] + z[q][k], e.act_param) - prev;   // Eq. 5
           mx = fmaxf(mx, fabsf(d));
         }
       }
@@ -212,8 +241,8 @@ __device__ __forceinline__ bool group_finish_pixel(const Epi& e, long long pix, 
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             sv[k] = a[q][k] + t[q][k] + z[q][k];
-            const float prev = first ? 0.f : act_f(e.act, a[q][k], e.act_param);
-            dv[k] = rnd<T>(act_f(e.act, sv[k], e.act_param) - prev);
+            const float prev = first ? 0.f : act_t<ACT>(a[q][k], e.act_param);
+            dv[k] = rnd<T>(act_t<ACT>(sv[k], e.act_param) - prev);
           }
           st8(A + 8 * j, sv);                                // Eq. 6
           st8_zero(Tt + 8 * j);

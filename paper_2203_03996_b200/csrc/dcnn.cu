@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -141,17 +142,26 @@ static dcnn_status plan_cc(Op& o) {
   return DCNN_OK;
 }
 
-static bool plan_tc(Op& o, int dtype, int flags) {
+static bool plan_tc(Op& o, int dtype, int flags, int S) {
   if (dtype != DCNN_F16 || (flags & DCNN_FLAG_NO_TENSOR_CORES)) return false;
   if (o.Ci % 16 || o.C > 512) return false;
   ConvTCParams& p = o.tcp;
   memset(&p, 0, sizeof(p));
   p.Np = (o.C + 15) / 16 * 16;
-  p.n_acc = p.Np <= 256 ? 2 : 1;
-  p.acc_stride = p.n_acc == 2 ? (p.Np + 31) / 32 * 32 : 0;
-  int cols = p.n_acc == 2 ? 2 * p.acc_stride : 512;
+  // split output channels over a cluster when the layer has few tiles (small maps,
+  // wide layers): every CTA then streams only its slice of the weights
+  const int ntiles = S * ((o.H + 15) / 16) * ((o.W + 7) / 8);
+  int ns = 1;
+  static const int max_split = getenv("DCNN_TC_MAX_SPLIT") ? atoi(getenv("DCNN_TC_MAX_SPLIT")) : 8;
+  while (ns < max_split && p.Np % (16 * ns * 2) == 0 && p.Np / (ns * 2) >= 32 && ntiles * ns * 2 <= 2 * 148) ns *= 2;
+  while (p.Np / ns > 256) ns *= 2;            // one MMA N <= 256 per CTA
+  if (p.Np % (16 * ns)) return false;
+  p.nsplit = ns;
+  p.Ns = p.Np / ns;
+  p.n_acc = 2;
+  p.acc_stride = (p.Ns + 31) / 32 * 32;
   int tc = 32;
-  while (tc < cols) tc *= 2;
+  while (tc < 2 * p.acc_stride) tc *= 2;
   p.tmem_cols = tc;
   const int s = o.stride, d = o.dil;
   p.HH = 15 * s + (o.kh - 1) * d + 1;
@@ -159,12 +169,12 @@ static bool plan_tc(Op& o, int dtype, int flags) {
   if (p.HH * p.WW > 1024) return false;                 // halo mask staging buffer
   const int WQ = (p.WW + s - 1) / s;
   p.WWp = s * WQ;
-  const size_t budget = 227 * 1024 - 384;
+  const size_t budget = 227 * 1024 - 384 - 1024 - 1024;
   for (int BK = 64; BK >= 16; BK /= 2) {
     if (o.Ci % BK) continue;
     const int plane = (p.HH * p.WWp * 16 + 127) / 128 * 128 + 16;
     const int a_bytes = ((BK / 8) * plane + 127) / 128 * 128;
-    const int b_bytes = p.Np * BK * 2;
+    const int b_bytes = p.Ns * BK * 2;
     if (2 * (size_t)a_bytes + 2 * (size_t)b_bytes > budget) continue;
     int stages = (int)((budget - 2 * (size_t)a_bytes) / b_bytes);
     if (stages > 8) stages = 8;
@@ -498,7 +508,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
     }
     if (o.kind == DCNN_OP_CONV) {
       if ((r = plan_cc(o))) return r;
-      o.tc = plan_tc(o, n->dtype, n->flags);
+      o.tc = plan_tc(o, n->dtype, n->flags, n->S);
       if (o.tc) { o.TH = 16; o.TW = 8; }
       o.K = o.kh * o.kw * (o.Ci / o.groups);
       o.nty = (o.H + o.TH - 1) / o.TH;
@@ -538,23 +548,30 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         p.kh = o.kh; p.kw = o.kw; p.stride = o.stride; p.pad = o.pad; p.dil = o.dil;
         p.nty = o.nty; p.ntx = o.ntx;
         p.bias = o.bias;
-        // weights -> the shared-memory image of every (channel block, tap) step:
-        // [ncb*kh*kw][BK/8][Np][8] fp16, K-major core matrices (8 rows x 16 B)
-        const int ntaps = o.kh * o.kw, nch = p.BK / 8;
-        std::vector<__half> w((size_t)p.ncb * ntaps * nch * p.Np * 8, __float2half(0.f));
-        for (int cb = 0; cb < p.ncb; ++cb)
-          for (int tap = 0; tap < ntaps; ++tap)
-            for (int ch = 0; ch < nch; ++ch)
-              for (int nn = 0; nn < o.C; ++nn)
-                for (int e = 0; e < 8; ++e) {
-                  const int ci = cb * p.BK + ch * 8 + e;
-                  const float v = wt[((size_t)tap * o.Ci + ci) * o.Cp + nn];   // dense-expanded groups
-                  w[((((size_t)(cb * ntaps + tap) * nch + ch) * p.Np + nn) * 8) + e] = __float2half_rn(v);
+        // weights -> the shared-memory image of every (channel block, tap) step of
+        // every channel split: [nsplit][ncb*kh*kw][BK/8][Ns][8] fp16, K-major core
+        // matrices (8 rows x 16 B)
+        const int ntaps = o.kh * o.kw, nch = p.BK / 8, nsteps = p.ncb * ntaps;
+        std::vector<__half> w((size_t)p.nsplit * nsteps * nch * p.Ns * 8, __float2half(0.f));
+        for (int r = 0; r < p.nsplit; ++r)
+          for (int cb = 0; cb < p.ncb; ++cb)
+            for (int tap = 0; tap < ntaps; ++tap)
+              for (int ch = 0; ch < nch; ++ch)
+                for (int nl = 0; nl < p.Ns; ++nl) {
+                  const int nn = r * p.Ns + nl;
+                  if (nn >= o.C) continue;
+                  for (int e = 0; e < 8; ++e) {
+                    const int ci = cb * p.BK + ch * 8 + e;
+                    const float v = wt[((size_t)tap * o.Ci + ci) * o.Cp + nn];   // dense-expanded groups
+                    w[((((size_t)r * nsteps + cb * ntaps + tap) * nch + ch) * p.Ns + nl) * 8 + e] =
+                        __float2half_rn(v);
+                  }
                 }
         if ((r = dalloc(n, &o.wtc, w.size() * 2))) return r;
         CUDA_TRY(cudaMemcpy(o.wtc, w.data(), w.size() * 2, cudaMemcpyHostToDevice));
         p.wtc = o.wtc;
-        o.grid_tc = std::max(1, std::min(n->S * o.nty * o.ntx, 148));
+        const int ncl = std::max(1, std::min(n->S * o.nty * o.ntx, 148 / p.nsplit));
+        o.grid_tc = ncl * p.nsplit;
       }
     }
     if (o.kind == DCNN_OP_AFFINE) {

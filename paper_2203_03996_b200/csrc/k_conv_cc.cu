@@ -94,7 +94,7 @@ size_t conv_cc_smem(const ConvCCParams& p) {
   return win + msk + zt;
 }
 
-template <typename T, typename TC>
+template <typename T, typename TC, int ACT>
 __global__ void __launch_bounds__(CC_THREADS) k_conv_cc(ConvCCParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   float* win = reinterpret_cast<float*>(smem);
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(CC_THREADS) k_conv_cc(ConvCCParams p) {
         const long long pix = ((long long)s * p.Ho + oy) * p.Wo + ox;
         const bool valid = pl < P && oy < p.Ho && ox < p.Wo && p.ep.mask[pix];   // m_conv from a2
         const float* zr = zt + (size_t)pl * p.Cp;
-        const bool up = group_finish_pixel<T, TC>(p.ep, pix, valid, gl, G, [&](int j, float z[8]) {
+        const bool up = group_finish_pixel<T, TC, ACT>(p.ep, pix, valid, gl, G, [&](int j, float z[8]) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) z[k] = first ? zr[8 * j + k] + bias[8 * j + k] : zr[8 * j + k];
         });
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(CC_THREADS) k_conv_cc(ConvCCParams p) {
         const long long pix = ((long long)s * p.Ho + oy) * p.Wo + ox;
         if (!p.ep.mask[pix]) continue;         // m_conv from a2; skipped pixels stay 0
         const float* zr = zt + (size_t)pl * p.Cp;
-        const bool up = warp_finish_pixel<T, TC>(p.ep, pix, lane, [&](int c) {
+        const bool up = warp_finish_pixel<T, TC, ACT>(p.ep, pix, lane, [&](int c) {
           return first ? zr[c] + bias[c] : zr[c];
         });
         if (lane == 0 && up) ++nact;
@@ -223,22 +223,36 @@ __global__ void __launch_bounds__(CC_THREADS) k_conv_cc(ConvCCParams p) {
   warp_count_flush(p.ep.n_active, lane, nact);
 }
 
+template <typename T, typename TC>
+static cudaError_t cc_attr() {
+  cudaError_t err = cudaSuccess;
+  for (int a = 0; a <= ACT_SIGMOID; ++a)
+    act_dispatch(a, [&](auto A) {
+      cudaError_t e = cudaFuncSetAttribute(k_conv_cc<T, TC, decltype(A)::value>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e != cudaSuccess) err = e;
+    });
+  return err;
+}
+
 cudaError_t conv_cc_init() {
-  cudaError_t e = cudaFuncSetAttribute(k_conv_cc<__half, __half>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_conv_cc<__half, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_conv_cc<float, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaError_t e = cc_attr<__half, __half>();
+  if (e == cudaSuccess) e = cc_attr<__half, float>();
+  if (e == cudaSuccess) e = cc_attr<float, float>();
+  return e;
 }
 
 void launch_conv_cc(const ConvCCParams& p, int dtype, int cache32, int grid, cudaStream_t st) {
   const size_t smem = conv_cc_smem(p);
-  if (dtype == 1) {
-    if (cache32) k_conv_cc<__half, float><<<grid, CC_THREADS, smem, st>>>(p);
-    else k_conv_cc<__half, __half><<<grid, CC_THREADS, smem, st>>>(p);
-  } else {
-    k_conv_cc<float, float><<<grid, CC_THREADS, smem, st>>>(p);
-  }
+  act_dispatch(p.ep.act, [&](auto A) {
+    constexpr int ACT = decltype(A)::value;
+    if (dtype == 1) {
+      if (cache32) k_conv_cc<__half, float, ACT><<<grid, CC_THREADS, smem, st>>>(p);
+      else k_conv_cc<__half, __half, ACT><<<grid, CC_THREADS, smem, st>>>(p);
+    } else {
+      k_conv_cc<float, float, ACT><<<grid, CC_THREADS, smem, st>>>(p);
+    }
+  });
 }
 
 }  // namespace dcnn

@@ -28,7 +28,7 @@ namespace dcnn {
 constexpr int TC_THREADS = 320;
 
 struct TcSmem {                 // byte offsets inside dynamic shared memory
-  uint32_t bar, tmem_slot, hmask, a0, a1, b0;
+  uint32_t bar, tmem_slot, pmax, hmask, a0, a1, b0;
 };
 
 constexpr int TC_HMASK_BYTES = 1024;   // halo update mask of the current tile (u8)
@@ -37,8 +37,9 @@ __host__ __device__ inline TcSmem tc_layout(const ConvTCParams& p) {
   TcSmem L;
   L.bar = 0;                                  // up to 32 mbarriers
   L.tmem_slot = 32 * 8;
-  L.hmask = 384;
-  L.a0 = 384 + TC_HMASK_BYTES;
+  L.pmax = 384;                               // [2][128] f32 partial max-norms (cluster exchange)
+  L.hmask = L.pmax + 1024;
+  L.a0 = L.hmask + TC_HMASK_BYTES;
   L.a1 = L.a0 + p.a_bytes;
   L.b0 = L.a1 + p.a_bytes;
   return L;
@@ -49,7 +50,7 @@ size_t conv_tc_smem(const ConvTCParams& p) {
   return (size_t)L.b0 + (size_t)p.stages * p.b_bytes;
 }
 
-template <typename TC>
+template <typename TC, int ACT>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const TcSmem L = tc_layout(p);
@@ -61,13 +62,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
   uint64_t* a_empty = bars + 18;              // [2]
   uint64_t* acc_full = bars + 20;             // [2]
   uint64_t* acc_empty = bars + 22;            // [2]
+  uint64_t* xch = bars + 24;                  // [2] cluster max-norm exchange
+  float* pmax = reinterpret_cast<float*>(smem + L.pmax);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
   uint8_t* hmask = smem + L.hmask;
   unsigned char* abuf[2] = {smem + L.a0, smem + L.a1};
   unsigned char* bstage = smem + L.b0;
 
   const int count = *p.count;
-  if ((int)blockIdx.x >= count) return;       // uniform: no tile for this CTA
+  // a cluster of nsplit CTAs shares each tile; CTA `rank` owns output channels
+  // [rank*Ns, rank*Ns+Ns).  Clusters iterate the tile list persistently.
+  const int nsplit = p.nsplit;
+  const int rank = nsplit > 1 ? (int)tc::cluster_rank() : 0;
+  const int cid = blockIdx.x / nsplit, ncl = gridDim.x / nsplit;
+  if (cid >= count) return;                   // uniform per cluster: no tile
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ntaps = p.kh * p.kw;
   const int nsteps = p.ncb * ntaps;
@@ -79,12 +87,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
       tc::mbar_init(&a_empty[i], 1);
       tc::mbar_init(&acc_full[i], 1);
       tc::mbar_init(&acc_empty[i], 128);
+      tc::mbar_init(&xch[i], nsplit);
     }
     tc::mbar_fence_init();
   }
   if (warp == 9) tc::tmem_alloc(tmem_slot, p.tmem_cols);
   tc::tc_fence_before();
-  __syncthreads();
+  if (nsplit > 1) tc::cluster_sync_all();     // remote arrivals need initialised barriers
+  else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -99,7 +109,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
     const int items = npx * nch;
     const int WQ = p.WWp / p.stride;
     int q = 0;                                 // global c-block counter (buffer ring)
-    for (int ti = blockIdx.x; ti < count; ti += gridDim.x) {
+    for (int ti = cid; ti < count; ti += ncl) {
       const int tile = p.list[ti];
       const int s = tile / (p.nty * p.ntx);
       const int ty = (tile / p.ntx) % p.nty, tx = tile % p.ntx;
@@ -134,13 +144,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
     // ---------------------------------------------------------------- weight producer
     if (lane == 0) {
       int j = 0;
-      for (int ti = blockIdx.x; ti < count; ti += gridDim.x) {
+      for (int ti = cid; ti < count; ti += ncl) {
         for (int st = 0; st < nsteps; ++st, ++j) {
           const int slot = j % p.stages;
           tc::mbar_wait(&b_empty[slot], ((j / p.stages) & 1) ^ 1);
           tc::mbar_arrive_expect_tx(&b_full[slot], p.b_bytes);
           tc::bulk_g2s(bstage + (size_t)slot * p.b_bytes,
-                       reinterpret_cast<const unsigned char*>(p.wtc) + (size_t)st * p.b_bytes, p.b_bytes,
+                       reinterpret_cast<const unsigned char*>(p.wtc) + ((size_t)rank * nsteps + st) * p.b_bytes,
+                       p.b_bytes,
                        &b_full[slot]);
         }
       }
@@ -149,10 +160,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       const uint32_t sbo_a = (uint32_t)(p.stride * p.WWp * 16);
-      const uint32_t lbo_b = (uint32_t)(p.Np * 16);
+      const uint32_t lbo_b = (uint32_t)(p.Ns * 16);
       const int WQ = p.WWp / p.stride;
       int j = 0, q = 0, u = 0;
-      for (int ti = blockIdx.x; ti < count; ti += gridDim.x, ++u) {
+      for (int ti = cid; ti < count; ti += ncl, ++u) {
         const int acc = u % p.n_acc;
         tc::mbar_wait(&acc_empty[acc], ((u / p.n_acc) & 1) ^ 1);
         tc::tc_fence_after();
@@ -171,9 +182,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
             const uint32_t bbase = tc::smem_u32(bstage + (size_t)slot * p.b_bytes);
             for (int kc = 0; kc < p.BK / 16; ++kc) {
               const uint64_t ad = tc::smem_desc(abase + (uint32_t)(2 * kc * p.plane + toff * 16), p.plane, sbo_a);
-              for (int nc = 0; nc * 256 < p.Np; ++nc) {
-                const int nn = min(256, p.Np - nc * 256);
-                const uint64_t bd = tc::smem_desc(bbase + (uint32_t)(2 * kc * p.Np * 16 + nc * 256 * 16), lbo_b, 128);
+              for (int nc = 0; nc * 256 < p.Ns; ++nc) {
+                const int nn = min(256, p.Ns - nc * 256);
+                const uint64_t bd = tc::smem_desc(bbase + (uint32_t)(2 * kc * p.Ns * 16 + nc * 256 * 16), lbo_b, 128);
                 tc::mma_f16(dbase + nc * 256, ad, bd, tc::idesc_f16(128, nn), (cb | tap | kc) != 0);
               }
             }
@@ -189,12 +200,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
     // thread = TMEM lane = output pixel; Eqs. 4-6 with the per-pixel max-norm
     // computed in registers (pass 1), then caches / delta / output written (pass 2).
     const Epi& e = p.ep;
-    const int C = e.C;
-    const bool vec = (C % 8) == 0;
+    const int Cg = e.C;                       // channels of the output rows (pitch)
+    const int cb0 = rank * p.Ns;              // this CTA's first output channel
+    const int C = min(p.Ns, Cg - cb0);        // this CTA's channels
+    const bool vec = (Cg % 8) == 0;
     const float eps = *e.eps;
+    const float* bias = p.bias + cb0;
     unsigned nact = 0;
     int u = 0;
-    for (int ti = blockIdx.x; ti < count; ti += gridDim.x, ++u) {
+    for (int ti = cid; ti < count; ti += ncl, ++u) {
       const int tile = p.list[ti];
       const int s = tile / (p.nty * p.ntx);
       const int ty = (tile / p.ntx) % p.nty, tx = tile % p.ntx;
@@ -207,102 +221,133 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
       tc::mbar_wait(&acc_full[acc], (u / p.n_acc) & 1);
       tc::tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * p.acc_stride);
-      __half* dl = reinterpret_cast<__half*>(e.delta) + pix * C;
-      float* O = e.O ? e.O + pix * C : nullptr;
-      TC* A = reinterpret_cast<TC*>(e.xA) + pix * C;
-      TC* Tt = reinterpret_cast<TC*>(e.xT) + pix * C;
-      const bool trunc = e.act != ACT_NONE;
+      __half* dl = reinterpret_cast<__half*>(e.delta) + pix * Cg + cb0;
+      float* O = e.O ? e.O + pix * Cg + cb0 : nullptr;
+      TC* A = reinterpret_cast<TC*>(e.xA) + pix * Cg + cb0;
+      TC* Tt = reinterpret_cast<TC*>(e.xT) + pix * Cg + cb0;
+      constexpr bool trunc = ACT != ACT_NONE;
       bool upd = act;
-      // load 16 channels of z (+bias on the first frame), x^A, x^T
-      auto fetch = [&](int c0, float z[16], float a[16], float t[16]) {
-        uint32_t r[16];
-        tc::tmem_ld16(tbase + c0, r);
+      // 32 channels per step: two TMEM loads, one wait, and all cache loads of the
+      // group issued back to back (8 x 16 B in flight per thread)
+      auto fetch = [&](int c0, float z[32], float a[32], float t[32]) {
+        uint32_t r0[16], r1[16];
+        tc::tmem_ld16(tbase + c0, r0);
+        tc::tmem_ld16(tbase + c0 + 16, r1);
         tc::tmem_wait_ld();
         if (!act) return;
+        const bool full = vec && c0 + 32 <= C;
+        if (trunc && !first) {
+          if (full) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) z[k] = __uint_as_float(r[k]) + ((first && c0 + k < C) ? p.bias[c0 + k] : 0.f);
-        if (!trunc) return;
-        if (first) {
+            for (int k = 0; k < 32; k += 8) { ld8(A + c0 + k, a + k); ld8(Tt + c0 + k, t + k); }
+          } else {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) a[k] = t[k] = 0.f;
-        } else if (vec && c0 + 16 <= C) {
-          ld8(A + c0, a); ld8(A + c0 + 8, a + 8);
-          ld8(Tt + c0, t); ld8(Tt + c0 + 8, t + 8);
+            for (int k = 0; k < 32; ++k) {
+              a[k] = c0 + k < C ? ld(A + c0 + k) : 0.f;
+              t[k] = c0 + k < C ? ld(Tt + c0 + k) : 0.f;
+            }
+          }
         } else {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            a[k] = c0 + k < C ? ld(A + c0 + k) : 0.f;
-            t[k] = c0 + k < C ? ld(Tt + c0 + k) : 0.f;
-          }
+          for (int k = 0; k < 32; ++k) a[k] = t[k] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          z[k] = __uint_as_float(r0[k]);
+          z[k + 16] = __uint_as_float(r1[k]);
+        }
+        if (first) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) z[k] += c0 + k < C ? bias[c0 + k] : 0.f;
         }
       };
       if (trunc) {
         float mx = 0.f;
-        for (int c0 = 0; c0 < C; c0 += 16) {
-          float z[16], a[16], t[16];
+        for (int c0 = 0; c0 < C; c0 += 32) {
+          float z[32], a[32], t[32];
           fetch(c0, z, a, t);
           if (act) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k)
+            for (int k = 0; k < 32; ++k)
               if (c0 + k < C) {
-                const float prev = first ? 0.f : act_f(e.act, a[k], e.act_param);
-                mx = fmaxf(mx, fabsf(act_f(e.act, a[k] + t[k] + z[k], e.act_param) - prev));
+                const float prev = first ? 0.f : act_t<ACT>(a[k], e.act_param);
+                mx = fmaxf(mx, fabsf(act_t<ACT>(a[k] + t[k] + z[k], e.act_param) - prev));
               }
           }
         }
+        if (nsplit > 1) {
+          // per-pixel max-norm over all output channels of the cluster (DSMEM exchange)
+          const int xb = u & 1;
+          pmax[xb * 128 + tid] = mx;
+          tc::named_bar_sync(2, 128);
+          if (tid == 0) {
+            const uint32_t local = tc::smem_u32(&xch[xb]);
+            for (int r = 0; r < nsplit; ++r) tc::mbar_arrive_remote(tc::mapa(local, (uint32_t)r));
+          }
+          tc::mbar_wait_cluster(&xch[xb], (u >> 1) & 1);
+          const uint32_t mine = tc::smem_u32(&pmax[xb * 128 + tid]);
+          for (int r = 0; r < nsplit; ++r) mx = fmaxf(mx, tc::ld_dsmem_f32(tc::mapa(mine, (uint32_t)r)));
+        }
         upd = act && (first || eps < 0.f || mx > eps);
       }
-      for (int c0 = 0; c0 < C; c0 += 16) {
-        float z[16], a[16], t[16];
+      for (int c0 = 0; c0 < C; c0 += 32) {
+        float z[32], a[32], t[32];
         fetch(c0, z, a, t);
         if (!act) continue;
-        float o[16];          // values to store: delta (upd / linear) or new x^T
-        float sv[16];
+        const bool full = vec && c0 + 32 <= C;
+        if (trunc && !upd) {                                                  // x^T += dx
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          if (!trunc) {
-            o[k] = __half2float(__float2half_rn(z[k]));
-          } else if (upd) {
-            sv[k] = a[k] + t[k] + z[k];                                       // Eq. 6
-            const float prev = first ? 0.f : act_f(e.act, a[k], e.act_param);
-            o[k] = __half2float(__float2half_rn(act_f(e.act, sv[k], e.act_param) - prev));
+          for (int k = 0; k < 32; ++k) t[k] += z[k];
+          if (full) {
+#pragma unroll
+            for (int k = 0; k < 32; k += 8) st8(Tt + c0 + k, t + k);
           } else {
-            o[k] = t[k] + z[k];                                               // x^T += dx
+            for (int k = 0; k < 32 && c0 + k < C; ++k) st(Tt + c0 + k, t[k]);
           }
-        }
-        const bool full = vec && c0 + 16 <= C;
-        if (trunc && !upd) {
-          if (full) { st8(Tt + c0, o); st8(Tt + c0 + 8, o + 8); }
-          else for (int k = 0; k < 16 && c0 + k < C; ++k) st(Tt + c0 + k, o[k]);
           continue;
         }
-        if (full) {
-          st8(dl + c0, o); st8(dl + c0 + 8, o + 8);
+        float o[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
           if (trunc) {
-            st8(A + c0, sv); st8(A + c0 + 8, sv + 8);
-            st8_zero(Tt + c0); st8_zero(Tt + c0 + 8);
+            const float sv = a[k] + t[k] + z[k];                                // Eq. 6
+            const float prev = first ? 0.f : act_t<ACT>(a[k], e.act_param);
+            o[k] = __half2float(__float2half_rn(act_t<ACT>(sv, e.act_param) - prev));
+            a[k] = sv;
+          } else {
+            o[k] = __half2float(__float2half_rn(z[k]));
+          }
+        }
+        if (full) {
+#pragma unroll
+          for (int k = 0; k < 32; k += 8) {
+            st8(dl + c0 + k, o + k);
+            if (trunc) { st8(A + c0 + k, a + k); st8_zero(Tt + c0 + k); }
           }
           if (O) {
-            float ov[16];
             if (first) {
-              st8(O + c0, o); st8(O + c0 + 8, o + 8);
-            } else {
-              ld8(O + c0, ov); ld8(O + c0 + 8, ov + 8);
 #pragma unroll
-              for (int k = 0; k < 16; ++k) ov[k] += o[k];
-              st8(O + c0, ov); st8(O + c0 + 8, ov + 8);
+              for (int k = 0; k < 32; k += 8) st8(O + c0 + k, o + k);
+            } else {
+              float ov[32];
+#pragma unroll
+              for (int k = 0; k < 32; k += 8) ld8(O + c0 + k, ov + k);
+#pragma unroll
+              for (int k = 0; k < 32; ++k) ov[k] += o[k];
+#pragma unroll
+              for (int k = 0; k < 32; k += 8) st8(O + c0 + k, ov + k);
             }
           }
         } else {
-          for (int k = 0; k < 16 && c0 + k < C; ++k) {
+          for (int k = 0; k < 32 && c0 + k < C; ++k) {
             st(dl + c0 + k, o[k]);
-            if (trunc) { st(A + c0 + k, sv[k]); st(Tt + c0 + k, 0.f); }
+            if (trunc) { st(A + c0 + k, a[k]); st(Tt + c0 + k, 0.f); }
             if (O) O[c0 + k] = first ? o[k] : O[c0 + k] + o[k];
           }
         }
       }
-      if (act) e.mask[pix] = upd ? 1 : 0;
-      nact += upd ? 1 : 0;
+      if (act && rank == 0) e.mask[pix] = upd ? 1 : 0;
+      nact += (upd && rank == 0) ? 1 : 0;
       tc::tc_fence_before();
       tc::mbar_arrive(&acc_empty[acc]);
     }
@@ -310,22 +355,49 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
     unsigned n = (unsigned)warp_sum((int)nact);
     warp_count_flush(e.n_active, lane, n);
   }
-  __syncthreads();
+  if (nsplit > 1) tc::cluster_sync_all();     // partners may still read our smem
+  else __syncthreads();
   if (warp == 9) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, p.tmem_cols);
   }
 }
 
+template <typename TC>
+static cudaError_t tc_attr() {
+  cudaError_t err = cudaSuccess;
+  for (int a = 0; a <= ACT_SIGMOID; ++a)
+    act_dispatch(a, [&](auto A) {
+      cudaError_t e = cudaFuncSetAttribute(k_conv_tc<TC, decltype(A)::value>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) err = e;
+    });
+  return err;
+}
+
 cudaError_t conv_tc_init() {
-  cudaError_t e = cudaFuncSetAttribute(k_conv_tc<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_conv_tc<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaError_t e = tc_attr<__half>();
+  return e == cudaSuccess ? tc_attr<float>() : e;
 }
 
 void launch_conv_tc(const ConvTCParams& p, int cache32, int grid, cudaStream_t st) {
-  if (cache32) k_conv_tc<float><<<grid, TC_THREADS, conv_tc_smem(p), st>>>(p);
-  else k_conv_tc<__half><<<grid, TC_THREADS, conv_tc_smem(p), st>>>(p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = conv_tc_smem(p);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p.nsplit;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  act_dispatch(p.ep.act, [&](auto A) {
+    constexpr int ACT = decltype(A)::value;
+    if (cache32) cudaLaunchKernelEx(&cfg, k_conv_tc<float, ACT>, p);
+    else cudaLaunchKernelEx(&cfg, k_conv_tc<__half, ACT>, p);
+  });
 }
 
 }  // namespace dcnn

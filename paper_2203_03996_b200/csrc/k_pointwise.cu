@@ -6,12 +6,11 @@
 // pooling layers, upsampling layers, activations, concatenations and additions";
 // Eq. 3 for max-pool with an accumulated-input buffer (Z9).
 //
-// Work distribution: each warp owns 32 consecutive output pixels.  Lane i
-// computes the output mask of pixel i (coalesced u8 reads), the warp ballots,
-// writes 0 masks for inactive pixels, then finishes the active pixels 32/G at a
-// time: a group of G lanes per pixel, each lane moving 16-byte (fp16) / 32-byte
-// (fp32) channel chunks, so every NHWC row is read and written with full
-// sectors.  Inactive pixels cost one mask byte; their deltas are never touched
+// Work distribution: a group of G lanes (power of two <= min(32, C/8)) owns one
+// output pixel, so a warp works on 32/G pixels at once; each lane moves 16-byte
+// (fp16) / 32-byte (fp32) channel chunks, so every NHWC row is read and written
+// with full sectors and every pixel's loads are in flight together.  Kernels are
+// specialised per op kind and activation (compile-time f keeps the code small).  Inactive pixels cost one mask byte; their deltas are never touched
 // ("we do not need to initialize unprocessed values").
 #include "kernels.h"
 
@@ -180,7 +179,7 @@ __device__ __forceinline__ float pw_scalar(const PwParams& p, long long pix, int
   return sum / (float)(p.k * p.k);
 }
 
-template <typename T, typename TC, int KIND>
+template <typename T, typename TC, int KIND, int ACT>
 __global__ void __launch_bounds__(256) k_pointwise(PwParams p) {
   const int lane = threadIdx.x & 31;
   const long long npix = (long long)p.S * p.H * p.W;
@@ -190,35 +189,29 @@ __global__ void __launch_bounds__(256) k_pointwise(PwParams p) {
   const int G = p.vec ? p.G : 32;
   const int PPW = 32 / G, gi = lane / G, gl = lane % G;
   unsigned nact = 0;
-  for (long long base = gw * 32; base < npix; base += nw * 32) {
-    const long long pix = base + lane;
-    bool m = false;
-    if (pix < npix) {
-      const int s = (int)(pix / HWo);
-      m = pw_mask<KIND>(p, pix, s, p.ep.first[s] != 0);
-      if (!m) p.ep.mask[pix] = 0;
+  // warp w finishes pixels [w*PPW, w*PPW+PPW): one group of G lanes per pixel
+  for (long long base = gw * PPW; base < npix; base += nw * PPW) {
+    const long long q = base + gi;
+    bool valid = q < npix;
+    const int s = valid ? (int)(q / HWo) : 0;
+    const bool first = valid && p.ep.first[s] != 0;
+    if (valid) {
+      valid = pw_mask<KIND>(p, q, s, first);
+      if (!valid && gl == 0) p.ep.mask[q] = 0;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, m);
-    const int n = __popc(bal);
-    for (int r = 0; r < n; r += PPW) {
-      const int k = r + gi;
-      const bool valid = k < n;
-      const long long q = base + (valid ? (int)__fns(bal, 0, k + 1) : 0);
-      const int s = valid ? (int)(q / HWo) : 0;
-      const bool first = valid && p.ep.first[s] != 0;
-      bool mk[4];
+    if (!p.vec && !__any_sync(0xffffffffu, valid)) continue;   // warp-uniform (G = 32)
+    bool mk[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) mk[i] = valid && i < p.n_in && (first || p.min[i][q] != 0);
-      bool up;
-      if (p.vec) {
-        up = group_finish_pixel<T, TC>(p.ep, q, valid, gl, G,
-                                       [&](int j, float z[8]) { pw_chunk<T, TC, KIND>(p, q, s, first, mk, j, z); });
-      } else {
-        up = warp_finish_pixel<T, TC>(p.ep, q, lane,
-                                      [&](int c) { return pw_scalar<T, TC, KIND>(p, q, s, first, mk, c); });
-      }
-      if (valid && gl == 0 && up) ++nact;
+    for (int i = 0; i < 4; ++i) mk[i] = valid && i < p.n_in && (first || p.min[i][q] != 0);
+    bool up;
+    if (p.vec) {
+      up = group_finish_pixel<T, TC, ACT>(p.ep, q, valid, gl, G,
+                                     [&](int j, float z[8]) { pw_chunk<T, TC, KIND>(p, q, s, first, mk, j, z); });
+    } else {
+      up = warp_finish_pixel<T, TC, ACT>(p.ep, q, lane,
+                                    [&](int c) { return pw_scalar<T, TC, KIND>(p, q, s, first, mk, c); });
     }
+    if (valid && gl == 0 && up) ++nact;
   }
   const unsigned tot = (unsigned)warp_sum((int)nact);
   warp_count_flush(p.ep.n_active, lane, tot);
@@ -249,15 +242,20 @@ static int pw_grid(long long items, int per_block) {
 
 template <typename T, typename TC>
 static void pw_dispatch(const PwParams& p, cudaStream_t st) {
-  const int grid = pw_grid((long long)p.S * p.H * p.W, 256);
+  const int ppw = p.vec ? 32 / p.G : 1;                 // pixels per warp-iteration
+  const int grid = pw_grid(((long long)p.S * p.H * p.W + ppw - 1) / ppw, 8);
   switch (p.kind) {
-    case K_ACT: k_pointwise<T, TC, K_ACT><<<grid, 256, 0, st>>>(p); break;
-    case K_MAXPOOL: k_pointwise<T, TC, K_MAXPOOL><<<grid, 256, 0, st>>>(p); break;
-    case K_AVGPOOL: k_pointwise<T, TC, K_AVGPOOL><<<grid, 256, 0, st>>>(p); break;
-    case K_UP: k_pointwise<T, TC, K_UP><<<grid, 256, 0, st>>>(p); break;
-    case K_ADD: k_pointwise<T, TC, K_ADD><<<grid, 256, 0, st>>>(p); break;
-    case K_CONCAT: k_pointwise<T, TC, K_CONCAT><<<grid, 256, 0, st>>>(p); break;
-    case K_AFFINE: k_pointwise<T, TC, K_AFFINE><<<grid, 256, 0, st>>>(p); break;
+    case K_ACT:
+      act_dispatch(p.ep.act, [&](auto a) { k_pointwise<T, TC, K_ACT, decltype(a)::value><<<grid, 256, 0, st>>>(p); });
+      break;
+    case K_ADD:
+      act_dispatch(p.ep.act, [&](auto a) { k_pointwise<T, TC, K_ADD, decltype(a)::value><<<grid, 256, 0, st>>>(p); });
+      break;
+    case K_MAXPOOL: k_pointwise<T, TC, K_MAXPOOL, ACT_NONE><<<grid, 256, 0, st>>>(p); break;
+    case K_AVGPOOL: k_pointwise<T, TC, K_AVGPOOL, ACT_NONE><<<grid, 256, 0, st>>>(p); break;
+    case K_UP: k_pointwise<T, TC, K_UP, ACT_NONE><<<grid, 256, 0, st>>>(p); break;
+    case K_CONCAT: k_pointwise<T, TC, K_CONCAT, ACT_NONE><<<grid, 256, 0, st>>>(p); break;
+    case K_AFFINE: k_pointwise<T, TC, K_AFFINE, ACT_NONE><<<grid, 256, 0, st>>>(p); break;
   }
 }
 

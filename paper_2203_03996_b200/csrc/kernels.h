@@ -74,9 +74,10 @@ struct ConvTCParams {
   int a_bytes, b_bytes, stages; // halo buffer bytes, weight stage bytes, weight ring depth
   int n_acc, acc_stride;        // TMEM accumulators and their column stride
   int tmem_cols;
+  int nsplit, Ns;               // output channels split over a cluster of nsplit CTAs (Ns each)
   const __half* delta_in;
   const uint8_t* mask_in;
-  const __half* wtc;            // [ncb*kh*kw][BK/8][Np][8] fp16 (smem image of each step)
+  const __half* wtc;            // [nsplit][ncb*kh*kw][BK/8][Ns][8] fp16 (smem image of each step)
   const float* bias;
   const int* list; const int* count;
   Epi ep;

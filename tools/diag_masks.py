@@ -19,6 +19,8 @@ if dt == "f32":
     net.dtype = "f32"; fr = fr.astype(np.float32)
 if len(sys.argv) > 4 and sys.argv[4] == "c32":
     net.cache_dtype = "f32"
+if len(sys.argv) > 5:
+    net.set_inner_eps(float(sys.argv[5]))
 eng = DeltaNet(net, 1, flags=flags)
 orc = DeltaOracle(net, 1)
 outs = [torch.empty((1,) + s, device="cuda") for s in eng.out_shapes]
