@@ -246,6 +246,192 @@ def run_reference(args, wl, rank, world):
 
 
 # ------------------------------------------------------------------------- engine arm
+def run_engine(args, wl, wname, ctx, full=True):
+    """Time `args.steps` frames of workload `wl` on this rank; returns a result dict."""
+    import torch
+    from paper_2203_03996_b200 import (DeltaNet, KCLASS_CONV, KCLASS_TILES, KCLASS_POINTWISE,
+                                       KCLASS_INPUT)
+    rank, world, local, dist = ctx["rank"], ctx["world"], ctx["local"], ctx["dist"]
+    dev = torch.device("cuda", local)
+    net = wl["build"](args.dtype)
+    S = wl["S"]
+    npdt = np.float16 if args.dtype == "f16" else np.float32
+    tdt = torch.float16 if args.dtype == "f16" else torch.float32
+    steps = args.steps if full else max(5, args.steps // 3)
+    T = args.warmup + steps + 1
+    frames_np = make_frames(wl, S, T, rank, npdt)
+    frames = torch.from_numpy(frames_np).to(dev)              # inputs resident in HBM
+    stream = torch.cuda.current_stream(dev)
+    l2 = ctx["l2"]
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+
+    # ---- 1. headline: the frame graph exactly as a user runs it (no profiling events)
+    eng = DeltaNet(net, n_streams=S, device=local)
+    outs = [torch.empty((S,) + s, dtype=torch.float32, device=dev) for s in eng.out_shapes]
+    for t in range(args.warmup):
+        eng.process_frame(frames[t], outs, stream)
+    torch.cuda.synchronize()
+    step_ms = []
+    clock = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clock.start()
+    for k in range(steps):
+        flush_l2(l2)                                          # L2 flushed between timed steps
+        ev0.record(stream)
+        eng.process_frame(frames[args.warmup + k], outs, stream)
+        ev1.record(stream)
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+    torch.cuda.synchronize()
+    clocks = clock.stop()
+    total_ms = float(np.sum(step_ms))
+    if dist:
+        tt = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)             # max over ranks
+        total_ms = float(tt.item())
+    frames_all = S * world * steps
+    value = frames_all / (total_ms / 1e3)
+    kpf = eng.kernels_per_frame()
+    eng_last = [o.detach().double().cpu() for o in outs]
+    eng.close()
+
+    # ---- 2. profiling replay of the same frames: per-kernel-class device time + counters
+    engp = DeltaNet(net, n_streams=S, device=local)
+    classes = {"conv": KCLASS_CONV, "tiles": KCLASS_TILES, "pointwise": KCLASS_POINTWISE,
+               "input": KCLASS_INPUT}
+    engp.enable_kernel_timing(KCLASS_CONV | KCLASS_TILES | KCLASS_POINTWISE | KCLASS_INPUT)
+    for t in range(args.warmup):
+        engp.process_frame(frames[t], outs, stream)
+    dmacs = dense_macs(net) * S
+    kt = {k: [0.0, 0] for k in classes}
+    agg = {"mac_alg": 0, "mac_exec": 0, "tiles": 0, "tiles_proc": 0, "u_in": 0.0, "u_conv": 0.0}
+    conv_ops = [i for i, L in enumerate(net.layers) if L.op == "conv"]
+    for k in range(steps):
+        flush_l2(l2)
+        engp.process_frame(frames[args.warmup + k], outs, stream)
+        for name, c in classes.items():
+            ms, n = engp.kernel_timing(c)
+            kt[name][0] += ms
+            kt[name][1] += n
+        st = engp.stats()["ops"]
+        agg["u_in"] += st[0]["active_out"] / (S * net.in_h * net.in_w)
+        dens = []
+        for i in conv_ops:
+            r = st[i + 1]
+            agg["mac_alg"] += r["mac_alg"]
+            agg["mac_exec"] += r["mac_exec"]
+            agg["tiles"] += r["tiles_total"]
+            agg["tiles_proc"] += r["tiles_sparse"] + r["tiles_dense"]
+            Hs, Ws, _ = engp.op_shape(net.layers[i].inputs[0])
+            dens.append(r["active_in"] / (S * Hs * Ws))
+        agg["u_conv"] += float(np.mean(dens))
+    engp.close()
+    update = {"u_in": agg["u_in"] / steps, "u_conv": agg["u_conv"] / steps,
+              "mac_frac": agg["mac_alg"] / (dmacs * steps),
+              "mac_exec_frac": agg["mac_exec"] / (dmacs * steps),
+              "tiles_processed_frac": agg["tiles_proc"] / max(1, agg["tiles"])}
+
+    # ---- roofline of the dominant kernel class (delta conv)
+    pk = peaks()
+    conv_ms, conv_n = kt["conv"]
+    alg_flops = 2.0 * agg["mac_alg"]
+    per_launch_flops = alg_flops / max(1, conv_n)
+    avg_launch_s = conv_ms / 1e3 / max(1, conv_n)
+    tc = args.dtype == "f16"          # fp16 convs run on the tcgen05 path (fp32 on CUDA cores)
+    if tc:
+        # fp16 dense tensor rate = bf16 rate (B200_PROFILING.md); kernel timed inside a long step
+        peak = pk["bf16_tflops_sustained"]
+        bound, unit = "tensor", "TFLOP/s"
+    else:
+        # CUDA-core FFMA: 148 SMs x 128 fp32 lanes x 2 FLOP x max SM clock (DESIGN.md)
+        peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        bound, unit = "alu", "TFLOP/s"
+    achieved = per_launch_flops / avg_launch_s / 1e12 if avg_launch_s > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(wname, {}).get("conv_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                "frac": achieved / peak if peak else None, "traffic": traffic,
+                "kernel": ("delta conv (k_conv_tc tcgen05 + k_conv_cc very-sparse tiles)" if tc
+                           else "delta conv (k_conv_cc, FFMA)"),
+                "flops": "2 x kh*kw*Cin/g*Cout per pre-truncation active output pixel (mac_alg)",
+                "launches_per_step": conv_n / max(1, steps),
+                "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (fp16 = bf16 rate)" if tc else
+                                "148 SM x 128 FFMA lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)")}
+
+    # ---- dense baseline: PyTorch/cuDNN, channels_last, CUDA graph, same S and frames
+    dense = None
+    if not args.no_dense:
+        torch.backends.cudnn.benchmark = True
+        model = dense_module(net, torch).to(dev, tdt).to(memory_format=torch.channels_last)
+        xin = frames.permute(0, 1, 4, 2, 3)                   # [T,S,C,H,W] view
+        static_x = xin[0].contiguous(memory_format=torch.channels_last)
+        with torch.no_grad():
+            for _ in range(3):
+                model(static_x)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                static_out = model(static_x)
+            dms = []
+            for k in range(steps):
+                static_x.copy_(xin[args.warmup + k])
+                flush_l2(l2)
+                ev0.record(stream)
+                g.replay()
+                ev1.record(stream)
+                ev1.synchronize()
+                dms.append(ev0.elapsed_time(ev1))
+            torch.cuda.synchronize()
+        dense_fps = S * steps / (np.sum(dms) / 1e3)
+        dev_max = 0.0
+        for a, b in zip(eng_last, static_out):               # last timed frame
+            bb = b.float().permute(0, 2, 3, 1).cpu().double()
+            dev_max = max(dev_max, float((a - bb).abs().max() / bb.abs().max().clamp_min(1e-12)))
+        dense = {"fps": dense_fps, "ms_per_step": float(np.mean(dms)),
+                 "speedup": value / world / dense_fps, "deviation_vs_dense": dev_max,
+                 "impl": "torch cuDNN channels_last + CUDA graph (same weights, frames, streams)"}
+    res = {"value": value, "total_ms": total_ms, "steps": steps, "S": S, "net": net,
+           "frames_np": frames_np, "step_ms": step_ms, "clocks": clocks, "kpf": kpf,
+           "update": update, "roofline": roofline, "dense": dense,
+           "kernel_ms_per_step": {k: v[0] / steps for k, v in kt.items()}}
+
+    # ---- e2e through the C ABI with HOST buffers (H2D of the frame, D2H of the outputs)
+    if full:
+        eng2 = DeltaNet(net, n_streams=S, device=local)
+        host_frames = torch.from_numpy(frames_np).pin_memory()
+        host_outs = [torch.empty((S,) + s, dtype=torch.float32).pin_memory() for s in eng2.out_shapes]
+        hf = [host_frames[t].numpy() for t in range(T)]
+        ho = [o.numpy() for o in host_outs]
+        for t in range(args.warmup):
+            eng2.process_frame_host(hf[t], ho, stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ev0.record(stream)
+        for k in range(steps):
+            eng2.process_frame_host(hf[args.warmup + k], ho, stream)
+        ev1.record(stream)
+        ev1.synchronize()
+        e2e_ms = ev0.elapsed_time(ev1)
+        if dist:
+            tt = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
+        res["e2e"] = {"value": frames_all / (e2e_ms / 1e3), "unit": "frames/s",
+                      "h2d_bytes_per_step": int(frames_np[0].nbytes),
+                      "d2h_bytes_per_step": int(sum(o.nbytes for o in ho))}
+        eng2.close()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -257,6 +443,7 @@ def main():
     ap.add_argument("--streams", type=int, default=0, help="streams per GPU (default: workload's)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other workloads (N=1 only)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     wl = WORKLOADS[args.workload]
@@ -277,201 +464,60 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = {"rank": rank, "world": world, "local": local, "dist": dist,
+           "l2": torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32,
+                             device=torch.device("cuda", local))}   # 256 MiB > 126 MB L2
 
-    from paper_2203_03996_b200 import DeltaNet, KCLASS_CONV, KCLASS_TILES, KCLASS_POINTWISE, KCLASS_INPUT
+    r = run_engine(args, wl, args.workload, ctx, full=True)
+    net, S, steps = r["net"], r["S"], r["steps"]
 
-    net = wl["build"](args.dtype)
-    S = wl["S"]
-    npdt = np.float16 if args.dtype == "f16" else np.float32
-    tdt = torch.float16 if args.dtype == "f16" else torch.float32
-    T = args.warmup + args.steps + 1
-    frames_np = make_frames(wl, S, T, rank, npdt)
-    frames = torch.from_numpy(frames_np).cuda()               # inputs resident in HBM
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream(dev)
-
-    eng = DeltaNet(net, n_streams=S, device=local)
-    classes = {"conv": KCLASS_CONV, "tiles": KCLASS_TILES, "pointwise": KCLASS_POINTWISE,
-               "input": KCLASS_INPUT}
-    eng.enable_kernel_timing(KCLASS_CONV | KCLASS_TILES | KCLASS_POINTWISE | KCLASS_INPUT)
-    outs = [torch.empty((S,) + s, dtype=torch.float32, device=dev) for s in eng.out_shapes]
-    l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
-
-    for t in range(args.warmup):
-        eng.process_frame(frames[t], outs, stream)
-    torch.cuda.synchronize()
-
-    dmacs = dense_macs(net) * S
-    kt = {k: [0.0, 0] for k in classes}
-    agg = {"mac_alg": 0, "mac_exec": 0, "tiles": 0, "tiles_proc": 0, "u_in": 0.0, "u_conv": 0.0}
-    conv_ops = [i for i, L in enumerate(net.layers) if L.op == "conv"]
-    step_ms = []
-    clock = ClockSampler(local)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clock.start()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    for k in range(args.steps):
-        t = args.warmup + k
-        flush_l2(l2)
-        ev0.record(stream)
-        eng.process_frame(frames[t], outs, stream)
-        ev1.record(stream)
-        ev1.synchronize()
-        step_ms.append(ev0.elapsed_time(ev1))
-        for name, c in classes.items():
-            ms, n = eng.kernel_timing(c)
-            kt[name][0] += ms
-            kt[name][1] += n
-        st = eng.stats()["ops"]
-        in_px = S * net.in_h * net.in_w
-        agg["u_in"] += st[0]["active_out"] / in_px
-        dens = []
-        for i in conv_ops:
-            r = st[i + 1]
-            agg["mac_alg"] += r["mac_alg"]
-            agg["mac_exec"] += r["mac_exec"]
-            agg["tiles"] += r["tiles_total"]
-            agg["tiles_proc"] += r["tiles_sparse"] + r["tiles_dense"]
-            Hs, Ws, _ = eng.op_shape(net.layers[i].inputs[0])
-            dens.append(r["active_in"] / (S * Hs * Ws))
-        agg["u_conv"] += float(np.mean(dens))
-    torch.cuda.synchronize()
-    clocks = clock.stop()
-    total_ms = float(np.sum(step_ms))
-    if dist:
-        tt = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
-    frames_all = S * world * args.steps
-    value = frames_all / (total_ms / 1e3)
-
-    # --- roofline of the dominant kernel class (delta conv) ---------------------
-    pk = peaks()
-    conv_ms, conv_n = kt["conv"]
-    alg_flops = 2.0 * agg["mac_alg"]
-    per_launch_flops = alg_flops / max(1, conv_n)
-    avg_launch_s = conv_ms / 1e3 / max(1, conv_n)
-    tc = False
-    if tc:
-        peak = pk["bf16_tflops_sustained"]
-        bound, unit = "tensor", "TFLOP/s"
-    else:
-        # CUDA-core FFMA: 148 SMs x 128 fp32 lanes x 2 FLOP x max SM clock
-        peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        bound, unit = "alu", "TFLOP/s"
-    achieved = per_launch_flops / avg_launch_s / 1e12 if avg_launch_s > 0 else 0.0
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(args.workload, {}).get("conv_bytes_per_launch")
-        except Exception:
-            traffic = None
-    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-                "frac": achieved / peak if peak else None, "traffic": traffic,
-                "kernel": "delta conv (k_conv_cc)",
-                "peak_source": "148 SM x 128 FFMA lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)"}
-
-    # --- e2e through the C ABI with host buffers --------------------------------
-    eng2 = DeltaNet(net, n_streams=S, device=local)
-    host_frames = torch.from_numpy(frames_np).pin_memory()
-    host_outs = [torch.empty((S,) + s, dtype=torch.float32).pin_memory() for s in eng2.out_shapes]
-    hf = [host_frames[t].numpy() for t in range(T)]
-    ho = [o.numpy() for o in host_outs]
-    for t in range(args.warmup):
-        eng2.process_frame_host(hf[t], ho, stream)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for k in range(args.steps):
-        eng2.process_frame_host(hf[args.warmup + k], ho, stream)
-    e1.record(stream)
-    e1.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    if dist:
-        tt = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
-    e2e = {"value": frames_all / (e2e_ms / 1e3), "unit": "frames/s",
-           "h2d_bytes_per_step": int(frames_np[0].nbytes),
-           "d2h_bytes_per_step": int(sum(o.nbytes for o in ho))}
-    eng2.close()
-
-    # --- dense baseline: PyTorch/cuDNN fp16 channels_last, CUDA graph, same S ---
-    dense = None
-    if not args.no_dense:
-        torch.backends.cudnn.benchmark = True
-        model = dense_module(net, torch).to(dev, tdt).to(memory_format=torch.channels_last)
-        xin = frames[:, :, :, :, :].permute(0, 1, 4, 2, 3)       # [T,S,C,H,W] view
-        static_x = xin[0].contiguous(memory_format=torch.channels_last)
-        with torch.no_grad():
-            for _ in range(3):
-                model(static_x)
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                static_out = model(static_x)
-            dms = []
-            for k in range(args.steps):
-                static_x.copy_(xin[args.warmup + k])
-                flush_l2(l2)
-                ev0.record(stream)
-                g.replay()
-                ev1.record(stream)
-                ev1.synchronize()
-                dms.append(ev0.elapsed_time(ev1))
-        dense_fps = S * args.steps / (np.sum(dms) / 1e3)
-        # deviation of the sparse engine from dense inference at the last timed frame
-        eng_last = [o.cpu().double() for o in outs]
-        static_x.copy_(xin[args.warmup + args.steps - 1])
-        g.replay()
-        torch.cuda.synchronize()
-        dev_max = 0.0
-        for a, b in zip(eng_last, static_out):
-            bb = b.float().permute(0, 2, 3, 1).cpu().double()
-            dev_max = max(dev_max, float((a - bb).abs().max() / bb.abs().max().clamp_min(1e-12)))
-        dense = {"fps": dense_fps, "ms_per_step": float(np.mean(dms)), "speedup": value / world / dense_fps,
-                 "deviation_vs_dense": dev_max, "impl": "torch cuDNN fp16 channels_last + CUDA graph"}
-
-    # --- CPU oracle baseline (rank 0, N=1) ------------------------------------
+    # ---- CPU oracle baseline (rank 0, N=1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        fps, n, cores = cpu_oracle_time(net, frames_np[: min(T, 40)])
+        fps, n, cores = cpu_oracle_time(net, r["frames_np"][:40])
         cpu = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle",
                "sample": f"first {n} frames of the {args.workload} clip ({S} stream(s)), numpy fp64 oracle"}
 
-    kpf = eng.kernels_per_frame()
+    # ---- the other BASELINE workloads, reported beside the headline (N=1 only)
+    extra = {}
+    if world == 1 and not args.no_extra:
+        for wname, w2 in WORKLOADS.items():
+            if wname == args.workload:
+                continue
+            try:
+                r2 = run_engine(args, w2, wname, ctx, full=False)
+                extra[wname] = {"cfg": w2["cfg"], "fps": r2["value"],
+                                "dense_fps": r2["dense"]["fps"] if r2["dense"] else None,
+                                "speedup_vs_dense": r2["dense"]["speedup"] if r2["dense"] else None,
+                                "deviation_vs_dense": r2["dense"]["deviation_vs_dense"] if r2["dense"] else None,
+                                "update": r2["update"], "roofline_frac": r2["roofline"]["frac"],
+                                "kernels_per_frame": r2["kpf"], "steps": r2["steps"]}
+            except Exception as ex:   # report, never hide
+                extra[wname] = {"error": repr(ex)}
+
     line = {
-        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "metric": METRIC, "value": r["value"], "unit": "frames/s", "n_gpus": world,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": r["total_ms"] / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic",
         "config": {"workload": args.workload, "baseline_cfg": wl["cfg"], "model": wl["model"],
                    "streams_per_gpu": S, "frame": [net.in_h, net.in_w, 3],
                    "input_eps": net.input_eps, "input_dilation": net.input_dilation,
                    "inner_eps": max([L.eps for L in net.layers if L.truncates] + [0]),
-                   "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"streams x{world}"},
-        "update": {"u_in": agg["u_in"] / args.steps, "u_conv": agg["u_conv"] / args.steps,
-                   "mac_frac": agg["mac_alg"] / (dmacs * args.steps),
-                   "mac_exec_frac": agg["mac_exec"] / (dmacs * args.steps),
-                   "tiles_processed_frac": agg["tiles_proc"] / max(1, agg["tiles"])},
-        "dense": dense,
-        "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
-        "roofline": roofline,
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "parallelism": f"independent streams x{world} GPUs"},
+        "update": r["update"],
+        "dense": r["dense"],
+        "kernel_ms_per_step": r["kernel_ms_per_step"],
+        "roofline": r["roofline"],
         "cpu_baseline": cpu,
-        "e2e": e2e,
-        "gpu_launches": kpf * args.steps,
-        "kernels_per_frame": kpf,
-        "clocks": clocks,
-        "p50_ms": float(np.percentile(step_ms, 50)), "p99_ms": float(np.percentile(step_ms, 99)),
+        "e2e": r.get("e2e"),
+        "gpu_launches": r["kpf"] * steps,
+        "kernels_per_frame": r["kpf"],
+        "clocks": r["clocks"],
+        "p50_ms": float(np.percentile(r["step_ms"], 50)), "p99_ms": float(np.percentile(r["step_ms"], 99)),
+        "extra_workloads": extra,
     }
-    eng.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -6,7 +6,8 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdcnn.so")
+LIB_PATH = os.environ.get("DCNN_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                       "libdcnn.so")
 
 OP_CODES = {"conv": 0, "act": 1, "maxpool": 2, "avgpool": 3, "up": 4, "add": 5, "concat": 6,
             "affine": 7}

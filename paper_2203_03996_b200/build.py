@@ -16,8 +16,12 @@ FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-li
          "-Xptxas", "-warn-spills", "-I", os.path.join(HERE, "..", "include")]
 
 
+EXTRA = os.environ.get("DCNN_EXTRA_NVCC_FLAGS", "").split()
+SUFFIX = os.environ.get("DCNN_BUILD_SUFFIX", "")
+
+
 def _compile(src):
-    obj = os.path.join(CSRC, "build", os.path.basename(src) + ".o")
+    obj = os.path.join(CSRC, "build" + SUFFIX, os.path.basename(src) + ".o")
     dep_newer = False
     if os.path.exists(obj):
         t = os.path.getmtime(obj)
@@ -28,7 +32,7 @@ def _compile(src):
             dep_newer = True
     if os.path.exists(obj) and not dep_newer:
         return obj, ""
-    cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *FLAGS, *EXTRA, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -36,7 +40,7 @@ def _compile(src):
 
 
 def build(verbose=False):
-    os.makedirs(os.path.join(CSRC, "build"), exist_ok=True)
+    os.makedirs(os.path.join(CSRC, "build" + SUFFIX), exist_ok=True)
     srcs = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
     with cf.ThreadPoolExecutor(max_workers=8) as ex:
         res = list(ex.map(_compile, srcs))
@@ -45,12 +49,13 @@ def build(verbose=False):
             if err.strip():
                 print(err)
     objs = [o for o, _ in res]
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs,
+    lib = LIB if not SUFFIX else LIB.replace(".so", SUFFIX + ".so")
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib, *objs,
            "-Xcompiler", "-fPIC", "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

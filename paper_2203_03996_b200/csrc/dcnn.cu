@@ -158,6 +158,7 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
   if (p.Np % (16 * ns)) return false;
   p.nsplit = ns;
   p.Ns = p.Np / ns;
+  p.dbg = getenv("DCNN_TC_DBG") ? atoi(getenv("DCNN_TC_DBG")) : 0;
   p.n_acc = 2;
   p.acc_stride = (p.Ns + 31) / 32 * 32;
   int tc = 32;
@@ -169,23 +170,29 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
   if (p.HH * p.WW > 1024) return false;                 // halo mask staging buffer
   const int WQ = (p.WW + s - 1) / s;
   p.WWp = s * WQ;
-  const size_t budget = 227 * 1024 - 384 - 1024 - 1024;
+  const size_t budget = 226 * 1024 - 384 - 1024 - 1024;
+  const int ntaps = o.kh * o.kw;
+  // prefer wide K per weight stage (fewer mbarrier round trips), then more stages
   for (int BK = 64; BK >= 16; BK /= 2) {
     if (o.Ci % BK) continue;
     const int plane = (p.HH * p.WWp * 16 + 127) / 128 * 128 + 16;
     const int a_bytes = ((BK / 8) * plane + 127) / 128 * 128;
-    const int b_bytes = p.Ns * BK * 2;
-    if (2 * (size_t)a_bytes + 2 * (size_t)b_bytes > budget) continue;
-    int stages = (int)((budget - 2 * (size_t)a_bytes) / b_bytes);
-    if (stages > 8) stages = 8;
     if ((p.stride * p.WWp * 16) >> 4 >= (1 << 14) || plane >> 4 >= (1 << 14)) continue;
-    p.BK = BK;
-    p.ncb = o.Ci / BK;
-    p.plane = plane;
-    p.a_bytes = a_bytes;
-    p.b_bytes = b_bytes;
-    p.stages = stages;
-    return true;
+    for (int tg = ntaps; tg >= 1; --tg) {
+      if (ntaps % tg) continue;
+      const int b_bytes = tg * p.Ns * BK * 2;
+      if (2 * (size_t)a_bytes + 2 * (size_t)b_bytes > budget) continue;
+      int stages = (int)((budget - 2 * (size_t)a_bytes) / b_bytes);
+      if (stages > 8) stages = 8;
+      p.BK = BK;
+      p.ncb = o.Ci / BK;
+      p.plane = plane;
+      p.a_bytes = a_bytes;
+      p.b_bytes = b_bytes;
+      p.stages = stages;
+      p.tg = tg;
+      return true;
+    }
   }
   return false;
 }

@@ -22,10 +22,26 @@
 // warps 4-7 halo loaders, warp 8 weight producer, warp 9 TMEM alloc + MMA issuer.
 #include "kernels.h"
 #include "tc.cuh"
+#ifdef DCNN_TRACE
+#include <cstdio>
+#endif
 
 namespace dcnn {
 
 constexpr int TC_THREADS = 320;
+
+#ifdef DCNN_TRACE
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__shared__ unsigned long long g_tr[80];
+#define TRACE(cond, slot, t0) \
+  if ((cond) && blockIdx.x == 0) g_tr[slot] = gtime() - (t0)
+#else
+#define TRACE(cond, label, t0)
+#endif
 
 struct TcSmem {                 // byte offsets inside dynamic shared memory
   uint32_t bar, tmem_slot, pmax, hmask, a0, a1, b0;
@@ -69,6 +85,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
   unsigned char* abuf[2] = {smem + L.a0, smem + L.a1};
   unsigned char* bstage = smem + L.b0;
 
+#ifdef DCNN_TRACE
+  const unsigned long long t0 = gtime();
+#endif
   const int count = *p.count;
   // a cluster of nsplit CTAs shares each tile; CTA `rank` owns output channels
   // [rank*Ns, rank*Ns+Ns).  Clusters iterate the tile list persistently.
@@ -78,7 +97,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
   if (cid >= count) return;                   // uniform per cluster: no tile
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ntaps = p.kh * p.kw;
-  const int nsteps = p.ncb * ntaps;
+  const int ngroups = ntaps / p.tg;           // weight stages per channel block (tg taps each)
+  const int nsteps = p.ncb * ngroups;
 
   if (tid == 0) {
     for (int i = 0; i < p.stages; ++i) { tc::mbar_init(&b_full[i], 1); tc::mbar_init(&b_empty[i], 1); }
@@ -97,6 +117,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
   else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  TRACE(threadIdx.x == 0, 0, t0);
 
   if (warp >= 4 && warp < 8) {
     // ---------------------------------------------------------------- halo loaders
@@ -121,6 +142,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
         hmask[px] = (iy >= 0 && iy < p.H && ix >= 0 && ix < p.W) ? mi[iy * p.W + ix] : 0;
       }
       tc::named_bar_sync(1, 128);
+      TRACE(lt == 0 && ti == cid, 1, t0);
       const __half* src0 = p.delta_in + (long long)s * p.H * p.W * p.Ci;
       for (int cb = 0; cb < p.ncb; ++cb, ++q) {
         const int b = q & 1;
@@ -133,67 +155,88 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
           const bool v = hmask[px] != 0;
           const __half* g = v ? src0 + ((long long)(iy0 + hy) * p.W + (ix0 + hx)) * p.Ci + c0 + ch * 8 : src0;
           const int pi = hy * p.WWp + (hx % p.stride) * WQ + hx / p.stride;
-          tc::cp_async16(A + (uint32_t)(ch * p.plane + pi * 16), g, v);
+          if (!(p.dbg & 2)) tc::cp_async16(A + (uint32_t)(ch * p.plane + pi * 16), g, v);
         }
         tc::cp_async_wait_all();
         tc::fence_proxy_async_smem();          // generic-proxy writes -> tensor-core reads
         tc::mbar_arrive(&a_full[b]);
+        TRACE(lt == 0 && ti == cid && cb == 0, 2, t0);
       }
     }
   } else if (warp == 8) {
     // ---------------------------------------------------------------- weight producer
-    if (lane == 0) {
-      int j = 0;
-      for (int ti = cid; ti < count; ti += ncl) {
-        for (int st = 0; st < nsteps; ++st, ++j) {
-          const int slot = j % p.stages;
-          tc::mbar_wait(&b_empty[slot], ((j / p.stages) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&b_full[slot], p.b_bytes);
-          tc::bulk_g2s(bstage + (size_t)slot * p.b_bytes,
-                       reinterpret_cast<const unsigned char*>(p.wtc) + ((size_t)rank * nsteps + st) * p.b_bytes,
-                       p.b_bytes,
-                       &b_full[slot]);
+    // the whole warp runs the (warp-uniform) loop so the compiler keeps indices in
+    // uniform registers; one elected lane issues the bulk copies
+    int j = 0;
+    for (int ti = cid; ti < count; ti += ncl) {
+      for (int st = 0; st < nsteps; ++st, ++j) {
+        const int slot = j % p.stages;
+        tc::mbar_wait(&b_empty[slot], ((j / p.stages) & 1) ^ 1);
+        TRACE(j < 16 && lane == 0, 8 + j, t0);
+        if (tc::elect_one()) {
+          if (p.dbg & 1) {
+            tc::mbar_arrive(&b_full[slot]);
+          } else {
+            tc::mbar_arrive_expect_tx(&b_full[slot], p.b_bytes);
+            tc::bulk_g2s(bstage + (size_t)slot * p.b_bytes,
+                         reinterpret_cast<const unsigned char*>(p.wtc) + ((size_t)rank * nsteps + st) * p.b_bytes,
+                         p.b_bytes, &b_full[slot]);
+          }
         }
+        __syncwarp();
       }
     }
   } else if (warp == 9) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t sbo_a = (uint32_t)(p.stride * p.WWp * 16);
-      const uint32_t lbo_b = (uint32_t)(p.Ns * 16);
-      const int WQ = p.WWp / p.stride;
-      int j = 0, q = 0, u = 0;
-      for (int ti = cid; ti < count; ti += ncl, ++u) {
-        const int acc = u % p.n_acc;
-        tc::mbar_wait(&acc_empty[acc], ((u / p.n_acc) & 1) ^ 1);
+    // warp-uniform loop; descriptors live in uniform registers, one elected lane issues
+    const uint32_t sbo_a = (uint32_t)(p.stride * p.WWp * 16);
+    const uint32_t lbo_b = (uint32_t)(p.Ns * 16);
+    const int WQ = p.WWp / p.stride;
+    const uint32_t idesc = tc::idesc_f16(128, p.Ns);
+    int j = 0, q = 0, u = 0;
+    for (int ti = cid; ti < count; ti += ncl, ++u) {
+      const int acc = u % p.n_acc;
+      tc::mbar_wait(&acc_empty[acc], ((u / p.n_acc) & 1) ^ 1);
+      tc::tc_fence_after();
+      const uint32_t dbase = tmem + (uint32_t)(acc * p.acc_stride);
+      for (int cb = 0; cb < p.ncb; ++cb, ++q) {
+        const int b = q & 1;
+        tc::mbar_wait(&a_full[b], (q >> 1) & 1);
         tc::tc_fence_after();
-        const uint32_t dbase = tmem + (uint32_t)(acc * p.acc_stride);
-        for (int cb = 0; cb < p.ncb; ++cb, ++q) {
-          const int b = q & 1;
-          tc::mbar_wait(&a_full[b], (q >> 1) & 1);
+        TRACE(q < 8 && lane == 0, 40 + q, t0);
+        const uint32_t abase = tc::smem_u32(abuf[b]);
+        for (int g = 0; g < ngroups; ++g, ++j) {
+          const int slot = j % p.stages;
+          tc::mbar_wait(&b_full[slot], (j / p.stages) & 1);
           tc::tc_fence_after();
-          const uint32_t abase = tc::smem_u32(abuf[b]);
-          for (int tap = 0; tap < ntaps; ++tap, ++j) {
-            const int slot = j % p.stages;
-            tc::mbar_wait(&b_full[slot], (j / p.stages) & 1);
-            tc::tc_fence_after();
-            const int ky = tap / p.kw, kx = tap % p.kw;
-            const int toff = ky * p.dil * p.WWp + ((kx * p.dil) % p.stride) * WQ + (kx * p.dil) / p.stride;
-            const uint32_t bbase = tc::smem_u32(bstage + (size_t)slot * p.b_bytes);
-            for (int kc = 0; kc < p.BK / 16; ++kc) {
-              const uint64_t ad = tc::smem_desc(abase + (uint32_t)(2 * kc * p.plane + toff * 16), p.plane, sbo_a);
-              for (int nc = 0; nc * 256 < p.Ns; ++nc) {
-                const int nn = min(256, p.Ns - nc * 256);
-                const uint64_t bd = tc::smem_desc(bbase + (uint32_t)(2 * kc * p.Ns * 16 + nc * 256 * 16), lbo_b, 128);
-                tc::mma_f16(dbase + nc * 256, ad, bd, tc::idesc_f16(128, nn), (cb | tap | kc) != 0);
+          TRACE(j < 16 && lane == 0, 24 + j, t0);
+          const uint32_t bbase = tc::smem_u32(bstage + (size_t)slot * p.b_bytes);
+          if (tc::elect_one()) {
+            // all MMAs of tg taps x BK/16 K-steps against one weight stage
+            for (int t = 0; t < p.tg; ++t) {
+              const int tap = g * p.tg + t;
+              const int ky = tap / p.kw, kx = tap % p.kw;
+              const int toff = ky * p.dil * p.WWp + ((kx * p.dil) % p.stride) * WQ + (kx * p.dil) / p.stride;
+              const uint64_t ad0 = tc::smem_desc(abase + (uint32_t)(toff * 16), p.plane, sbo_a);
+              const uint64_t bd0 = tc::smem_desc(bbase + (uint32_t)(t * p.Ns * p.BK * 2), lbo_b, 128);
+              for (int kc = 0; kc < p.BK / 16; ++kc) {
+                // start-address fields advance by 2 planes (A) / 2 chunks (B) per K = 16
+                const uint64_t ad = ad0 + (uint64_t)((2 * kc * p.plane) >> 4);
+                const uint64_t bd = bd0 + (uint64_t)((2 * kc * p.Ns * 16) >> 4);
+                tc::mma_f16(dbase, ad, bd, idesc, (cb | tap | kc) != 0);
               }
             }
             tc::mma_commit(&b_empty[slot]);        // stage reusable once these MMAs finish
           }
-          tc::mma_commit(&a_empty[b]);             // halo buffer reusable
+          __syncwarp();
+          TRACE(j < 16 && lane == 0, 56 + j, t0);
         }
-        tc::mma_commit(&acc_full[acc]);            // accumulator ready for the epilogue
+        if (tc::elect_one()) tc::mma_commit(&a_empty[b]);   // halo buffer reusable
+        __syncwarp();
       }
+      if (tc::elect_one()) tc::mma_commit(&acc_full[acc]);  // accumulator ready for the epilogue
+      __syncwarp();
+      TRACE(ti == cid && lane == 0, 3, t0);
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 0-3)
@@ -220,6 +263,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
       const int acc = u % p.n_acc;
       tc::mbar_wait(&acc_full[acc], (u / p.n_acc) & 1);
       tc::tc_fence_after();
+      TRACE(tid == 0 && u == 0, 4, t0);
       const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * p.acc_stride);
       __half* dl = reinterpret_cast<__half*>(e.delta) + pix * Cg + cb0;
       float* O = e.O ? e.O + pix * Cg + cb0 : nullptr;
@@ -346,6 +390,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
           }
         }
       }
+      TRACE(tid == 0 && u == 0, 5, t0);
       if (act && rank == 0) e.mask[pix] = upd ? 1 : 0;
       nact += (upd && rank == 0) ? 1 : 0;
       tc::tc_fence_before();
@@ -357,6 +402,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
   }
   if (nsplit > 1) tc::cluster_sync_all();     // partners may still read our smem
   else __syncthreads();
+#ifdef DCNN_TRACE
+  TRACE(threadIdx.x == 0, 6, t0);
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    printf("[tc trace ns] setup %llu mask %llu halo0 %llu mma_issued %llu acc_ready %llu epi_done %llu end %llu\n",
+           g_tr[0], g_tr[1], g_tr[2], g_tr[3], g_tr[4], g_tr[5], g_tr[6]);
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    printf("  producer issue:");
+    for (int i = 0; i < 16; ++i) printf(" %llu", g_tr[8 + i]);
+    printf("\n  mma b_full ok:");
+    for (int i = 0; i < 16; ++i) printf(" %llu", g_tr[24 + i]);
+    printf("\n  mma issued   :");
+    for (int i = 0; i < 16; ++i) printf(" %llu", g_tr[56 + i]);
+    printf("\n  mma a_full ok:");
+    for (int i = 0; i < 8; ++i) printf(" %llu", g_tr[40 + i]);
+    printf("\n");
+  }
+#endif
   if (warp == 9) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, p.tmem_cols);
@@ -369,7 +431,7 @@ static cudaError_t tc_attr() {
   for (int a = 0; a <= ACT_SIGMOID; ++a)
     act_dispatch(a, [&](auto A) {
       cudaError_t e = cudaFuncSetAttribute(k_conv_tc<TC, decltype(A)::value>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
       if (e != cudaSuccess) err = e;
     });
   return err;

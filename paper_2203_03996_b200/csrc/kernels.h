@@ -72,9 +72,11 @@ struct ConvTCParams {
   int BK, ncb;                  // input channels per block, number of blocks
   int plane;                    // bytes per 8-channel plane of the halo buffer (= LBO of A)
   int a_bytes, b_bytes, stages; // halo buffer bytes, weight stage bytes, weight ring depth
+  int tg;                       // taps per weight stage (divides kh*kw)
   int n_acc, acc_stride;        // TMEM accumulators and their column stride
   int tmem_cols;
   int nsplit, Ns;               // output channels split over a cluster of nsplit CTAs (Ns each)
+  int dbg;                      // debug: bit0 skip weight copies, bit1 skip halo copies
   const __half* delta_in;
   const uint8_t* mask_in;
   const __half* wtc;            // [nsplit][ncb*kh*kw][BK/8][Ns][8] fp16 (smem image of each step)
