@@ -97,8 +97,11 @@ typedef struct {
 
 enum {
   DCNN_FLAG_NO_TENSOR_CORES = 1,  /* route every conv through the CUDA-core kernel      */
-  DCNN_FLAG_FP32_CACHES = 2       /* dtype F16: keep x^A, x^T and pool accumulators in
+  DCNN_FLAG_FP32_CACHES = 2,      /* dtype F16: keep x^A, x^T and pool accumulators in
                                      fp32 (deltas stay fp16)                             */
+  DCNN_FLAG_HYBRID_DISPATCH = 4   /* with tensor cores, route tiles with <= 4 active input
+                                     pixels to the CUDA-core kernel;
+                                     default: every non-empty tile on tcgen05             */
 };
 
 typedef struct {

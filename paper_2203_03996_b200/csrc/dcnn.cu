@@ -43,6 +43,7 @@ struct Op {
   int Hi = 0, Wi = 0, Ci = 0;       // shape of input 0
   int Cin[4] = {0, 0, 0, 0};
   int kh = 1, kw = 1, stride = 1, pad = 0, dil = 1, groups = 1, up = 1;
+  int Ci_real = 0;                  // input channels of the weights (Ci may be padded)
   int act = 0;
   float act_param = 0.1f;
   // device buffers
@@ -76,7 +77,7 @@ struct Op {
 
 struct dcnn_net {
   int device = 0, S = 1, dtype = 0, esz = 4, cache32 = 0, cesz = 4;
-  int inH = 0, inW = 0, inC = 0, radius = 0, flags = 0;
+  int inH = 0, inW = 0, inC = 0, inCp = 0, radius = 0, flags = 0;
   std::vector<Op> ops;
   std::vector<int> outputs;
   // device state
@@ -246,7 +247,7 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
   cudaMemsetAsync(n->stats, 0, sizeof(unsigned long long) * 8 * (nops + 1), st);
   if (n->n_counts) cudaMemsetAsync(n->counts, 0, sizeof(int) * n->n_counts, st);
   InputParams ip;
-  ip.S = n->S; ip.H = n->inH; ip.W = n->inW; ip.C = n->inC; ip.radius = n->radius;
+  ip.S = n->S; ip.H = n->inH; ip.W = n->inW; ip.C = n->inC; ip.Cp = n->inCp; ip.radius = n->radius;
   ip.frame = n->frame_in; ip.P = n->P; ip.delta = n->in_delta; ip.mask = n->in_mask;
   ip.eps = n->eps; ip.first = n->first; ip.err = n->err; ip.n_active = n->stats + 1;
   {
@@ -264,7 +265,9 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       tp.kh = o.kh; tp.kw = o.kw; tp.stride = o.stride; tp.pad = o.pad; tp.dil = o.dil;
       tp.TH = o.TH; tp.TW = o.TW; tp.nty = o.nty; tp.ntx = o.ntx;
       tp.mask_in = src_mask(o.in[0]); tp.mconv = o.mask; tp.first = n->first;
-      tp.sparse_max = 4; tp.use_tc = o.tc ? 1 : 0;
+      // hybrid dispatch: with tensor cores every non-empty tile runs on
+      // tcgen05 unless DCNN_FLAG_HYBRID_DISPATCH routes <= 4-active-input tiles to CUDA cores
+      tp.sparse_max = (n->flags & DCNN_FLAG_HYBRID_DISPATCH) ? 4 : 0; tp.use_tc = o.tc ? 1 : 0;
       tp.list_cc = o.list_cc; tp.count_cc = n->counts + o.cnt_idx;
       tp.list_tc = o.list_tc; tp.count_tc = n->counts + o.cnt_idx + 1;
       tp.stats = n->stats + (size_t)(i + 1) * 8;
@@ -285,11 +288,11 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       cp.vec = (o.C % 8 == 0) ? 1 : 0;
       cp.G = group_lanes(o.C);
       cp.ep = make_epi(n, i);
-      {
+      if (!o.tc || (n->flags & DCNN_FLAG_HYBRID_DISPATCH)) {
         TimeScope ts(n, st, DCNN_KCLASS_CONV);
         launch_conv_cc(cp, n->dtype, n->cache32, o.grid_cc, st);
+        ++k;
       }
-      ++k;
       if (o.tc) {
         ConvTCParams p = o.tcp;
         p.delta_in = reinterpret_cast<const __half*>(src_delta(o.in[0]));
@@ -464,6 +467,21 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
     if (o.H <= 0 || o.W <= 0 || o.C <= 0) return fail(DCNN_ERR_SHAPE, "layer " + std::to_string(i) + ": empty output");
     if (o.act != DCNN_ACT_NONE && o.C > 32 * MAXK) return fail(DCNN_ERR_UNSUPPORTED, "truncating op with more than 512 channels");
   }
+  // pad the input delta's channels to 16 when every consumer of the input is a
+  // dense conv that can then run on the tensor cores (zero channels, zero weights)
+  n->inCp = n->inC;
+  if (n->dtype == DCNN_F16 && !(n->flags & DCNN_FLAG_NO_TENSOR_CORES) && n->inC % 16) {
+    bool ok = true;
+    for (int i = 0; i < L; ++i)
+      for (int j = 0; j < n->ops[i].n_in; ++j)
+        if (n->ops[i].in[j] < 0 && (n->ops[i].kind != DCNN_OP_CONV || n->ops[i].groups != 1)) ok = false;
+    if (ok) n->inCp = (n->inC + 15) / 16 * 16;
+  }
+  for (int i = 0; i < L; ++i) {
+    Op& o = n->ops[i];
+    o.Ci_real = o.Ci;
+    if (o.in[0] < 0) o.Ci = n->inCp;
+  }
   for (int k = 0; k < d->n_outputs; ++k) {
     int j = d->output_ops[k];
     if (j < 0 || j >= L) return fail(DCNN_ERR_ARG, "output op index");
@@ -478,7 +496,8 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   dcnn_status r;
   if ((r = dalloc(n, &n->frame_in, n->frame_bytes))) return r;
   if ((r = dalloc(n, &n->P, n->frame_bytes))) return r;
-  if ((r = dalloc(n, &n->in_delta, n->frame_bytes))) return r;
+  if ((r = dalloc(n, &n->in_delta, in_px * n->inCp * es))) return r;
+  CUDA_TRY(cudaMemset(n->in_delta, 0, in_px * n->inCp * es));
   if ((r = dalloc(n, &n->in_mask, in_px))) return r;
   if ((r = dalloc(n, &n->first, S))) return r;
   if ((r = dalloc(n, &n->frame_idx, S * sizeof(long long)))) return r;
@@ -517,7 +536,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
       if ((r = plan_cc(o))) return r;
       o.tc = plan_tc(o, n->dtype, n->flags, n->S);
       if (o.tc) { o.TH = 16; o.TW = 8; }
-      o.K = o.kh * o.kw * (o.Ci / o.groups);
+      o.K = o.kh * o.kw * (o.Ci_real / o.groups);
       o.nty = (o.H + o.TH - 1) / o.TH;
       o.ntx = (o.W + o.TW - 1) / o.TW;
       const int ntiles = n->S * o.nty * o.ntx;
@@ -529,7 +548,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
       o.grid_cc = std::max(1, std::min(ntiles * nsub, 148 * 4));
       // weights: OHWI [Co][kh][kw][Ci/g] -> [kh*kw][Ci][Cp] fp32, groups expanded densely,
       // values rounded to the storage dtype (the method's weights are in dtype).
-      const int Cg = o.Ci / o.groups, Og = o.C / o.groups;
+      const int Cg = o.Ci_real / o.groups, Og = o.C / o.groups;
       std::vector<float> wt((size_t)o.kh * o.kw * o.Ci * o.Cp, 0.f);
       for (int co = 0; co < o.C; ++co) {
         const int g = co / Og;
@@ -738,7 +757,15 @@ dcnn_status dcnn_debug_read(dcnn_net* n, int32_t op, int32_t which, void* host, 
   if (op < 0) {
     const size_t px = (size_t)n->S * n->inH * n->inW;
     switch (which) {
-      case DCNN_BUF_DELTA: src = n->in_delta; nb = px * n->inC * es; break;
+      case DCNN_BUF_DELTA:
+        nb = px * n->inC * es;
+        if (bytes) *bytes = (int64_t)nb;
+        if (host) {
+          CUDA_TRY(cudaDeviceSynchronize());
+          CUDA_TRY(cudaMemcpy2D(host, n->inC * es, n->in_delta, n->inCp * es, n->inC * es, px,
+                                cudaMemcpyDeviceToHost));
+        }
+        return DCNN_OK;
       case DCNN_BUF_MASK: src = n->in_mask; nb = px; break;
       case DCNN_BUF_XA: src = n->P; nb = px * n->inC * es; break;
       default: return fail(DCNN_ERR_ARG, "buffer not present for the input layer");
@@ -795,7 +822,7 @@ dcnn_status dcnn_debug_poison(dcnn_net* n) {
   CUDA_TRY(cudaSetDevice(n->device));
   CUDA_TRY(cudaDeviceSynchronize());
   const size_t es = n->esz;
-  CUDA_TRY(cudaMemset(n->in_delta, 0xFF, (size_t)n->S * n->inH * n->inW * n->inC * es));
+  CUDA_TRY(cudaMemset2D(n->in_delta, n->inCp * es, 0xFF, n->inC * es, (size_t)n->S * n->inH * n->inW));
   for (auto& o : n->ops)
     CUDA_TRY(cudaMemset(o.delta, 0xFF, (size_t)n->S * o.H * o.W * o.C * es));
   CUDA_TRY(cudaDeviceSynchronize());

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) k_input(InputParams p) {
         for (int c = 0; c < C; ++c) {
           const float f = ld(F + pix * C + c);
           const float d = first ? f : f - ld(P + pix * C + c);
-          st(D + pix * C + c, d);
+          st(D + pix * p.Cp + c, d);
           st(P + pix * C + c, f);
         }
       }

@@ -13,6 +13,7 @@ namespace dcnn {
 // ---------------------------------------------------------------- a1: input
 struct InputParams {
   int S, H, W, C;
+  int Cp;                       // channel pitch of the delta buffer (>= C; pad channels stay 0)
   int radius;                   // Chebyshev dilation radius
   const void* frame;            // [S,H,W,C] T  (F, already in storage dtype)
   void* P;                      // [S,H,W,C] T  previous propagated input
