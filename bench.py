@@ -152,10 +152,26 @@ def dense_module(net, torch):
 
 
 # ------------------------------------------------------------------------- helpers
+def stream_seed(wl, rank, s):
+    """Streams are sharded across ranks: rank r owns global streams r*S .. r*S+S-1, each with its
+    own camera seed (distinct backgrounds and trajectories)."""
+    return wl["seed"] + 1000 * rank + s
+
+
+def max_over_ranks(x, dist, device=None):
+    """Device-timed durations are combined as the max over ranks (all-reduce MAX)."""
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def make_frames(wl, S, T, rank, dtype):
     v = wl["video"]
     vids = [Video(VideoSpec(v["H"], v["W"], 3, v["n_blobs"], v["blob_h"], v["blob_w"], v["speed"],
-                            v["noise_p"], False, wl["seed"] + 1000 * rank + s)) for s in range(S)]
+                            v["noise_p"], False, stream_seed(wl, rank, s))) for s in range(S)]
     return np.stack([np.stack([vv.frame(t, dtype) for vv in vids]) for t in range(T)])
 
 
@@ -284,11 +300,7 @@ def run_engine(args, wl, wname, ctx, full=True):
         step_ms.append(ev0.elapsed_time(ev1))
     torch.cuda.synchronize()
     clocks = clock.stop()
-    total_ms = float(np.sum(step_ms))
-    if dist:
-        tt = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)             # max over ranks
-        total_ms = float(tt.item())
+    total_ms = max_over_ranks(float(np.sum(step_ms)), dist, dev)
     frames_all = S * world * steps
     value = frames_all / (total_ms / 1e3)
     kpf = eng.kernels_per_frame()
@@ -417,11 +429,7 @@ def run_engine(args, wl, wname, ctx, full=True):
             eng2.process_frame_host(hf[args.warmup + k], ho, stream)
         ev1.record(stream)
         ev1.synchronize()
-        e2e_ms = ev0.elapsed_time(ev1)
-        if dist:
-            tt = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_ms = float(tt.item())
+        e2e_ms = max_over_ranks(ev0.elapsed_time(ev1), dist, dev)
         res["e2e"] = {"value": frames_all / (e2e_ms / 1e3), "unit": "frames/s",
                       "h2d_bytes_per_step": int(frames_np[0].nbytes),
                       "d2h_bytes_per_step": int(sum(o.nbytes for o in ho))}
