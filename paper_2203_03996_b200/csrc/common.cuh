@@ -11,6 +11,7 @@
 #include <stdint.h>
 
 #include <type_traits>
+#include <utility>
 
 namespace dcnn {
 
@@ -288,6 +289,42 @@ __device__ __forceinline__ bool group_finish_pixel(const Epi& e, long long pix, 
   }
   if (valid && gl == 0) e.mask[pix] = upd ? 1 : 0;
   return upd;
+}
+
+// Programmatic dependent launch (PDL): every kernel of the frame graph lets its
+// successor launch at once (so launch latency and the successor's data-independent
+// prologue overlap this kernel), and waits for its predecessors' completion and
+// memory flush before touching anything they produced.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// host: launch with the PDL attribute (and a cluster shape when cluster > 1)
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            int cluster, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = cluster;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // Flush a per-warp counter with one atomic (lane 0 holds the count).

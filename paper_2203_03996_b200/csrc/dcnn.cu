@@ -19,6 +19,11 @@
 
 using namespace dcnn;
 
+bool dcnn::pdl_enabled() {
+  static const bool on = getenv("DCNN_NO_PDL") == nullptr;
+  return on;
+}
+
 static thread_local std::string g_err;
 
 static dcnn_status fail(dcnn_status s, const std::string& msg) {
@@ -104,6 +109,10 @@ struct dcnn_net {
   // host staging for the _host entry point
   void* h_frames = nullptr;
   size_t frame_bytes = 0;
+  // branch streams used during graph capture
+  std::vector<cudaStream_t> aux;
+  std::vector<cudaEvent_t> ev_done, ev_join;
+  cudaEvent_t ev_fork = nullptr, ev_input = nullptr;
   // kernel timing (profiling)
   int timing_mask = 0;
   struct Timed { int cls; cudaEvent_t a, b; };
@@ -255,10 +264,43 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
     launch_input(ip, n->dtype, st);
   }
   ++k;
+  if (!n->aux.empty()) cudaEventRecord(n->ev_input, st);
   auto src_delta = [&](int j) -> const void* { return j < 0 ? n->in_delta : n->ops[j].delta; };
   auto src_mask = [&](int j) -> const uint8_t* { return j < 0 ? n->in_mask : n->ops[j].mask; };
+  // Independent branches (HRNet's parallel resolutions, YOLOv5s' C3 paths) are
+  // captured on separate streams so the graph runs them concurrently: an op continues
+  // the stream of a producer whose chain it extends, otherwise takes the least recently
+  // used stream; cross-stream inputs become event edges.
+  const int NS = (int)n->aux.size();
+  std::vector<int> op_stream(nops, 0);
+  std::vector<int> tail(NS + 1, -1);           // last op captured on each stream (0 = st)
+  auto stream_of = [&](int k2) -> cudaStream_t { return k2 == 0 ? st : n->aux[k2 - 1]; };
+  if (NS) {
+    cudaEventRecord(n->ev_fork, st);
+    for (int k2 = 0; k2 < NS; ++k2) cudaStreamWaitEvent(n->aux[k2], n->ev_fork, 0);
+  }
   for (int i = 0; i < nops; ++i) {
     Op& o = n->ops[i];
+    int sidx = -1;
+    for (int j = 0; j < o.n_in && sidx < 0; ++j) {
+      const int pj = o.in[j];
+      const int ps = pj < 0 ? 0 : op_stream[pj];
+      if (tail[ps] == pj) sidx = ps;
+    }
+    if (sidx < 0) {
+      sidx = 0;
+      for (int k2 = 1; k2 <= NS; ++k2)
+        if (tail[k2] < tail[sidx]) sidx = k2;
+    }
+    for (int j = 0; j < o.n_in; ++j) {
+      const int pj = o.in[j];
+      const int ps = pj < 0 ? 0 : op_stream[pj];
+      if (ps != sidx && pj >= 0) cudaStreamWaitEvent(stream_of(sidx), n->ev_done[pj], 0);
+      if (ps != sidx && pj < 0) cudaStreamWaitEvent(stream_of(sidx), n->ev_input, 0);
+    }
+    op_stream[i] = sidx;
+    tail[sidx] = i;
+    cudaStream_t ost = stream_of(sidx);
     if (o.kind == DCNN_OP_CONV) {
       TileParams tp;
       tp.S = n->S; tp.H = o.Hi; tp.W = o.Wi; tp.Ho = o.H; tp.Wo = o.W;
@@ -272,8 +314,8 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       tp.list_tc = o.list_tc; tp.count_tc = n->counts + o.cnt_idx + 1;
       tp.stats = n->stats + (size_t)(i + 1) * 8;
       {
-        TimeScope ts(n, st, DCNN_KCLASS_TILES);
-        launch_tiles(tp, st);
+        TimeScope ts(n, ost, DCNN_KCLASS_TILES);
+        launch_tiles(tp, ost);
       }
       ++k;
       ConvCCParams cp;
@@ -289,8 +331,8 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       cp.G = group_lanes(o.C);
       cp.ep = make_epi(n, i);
       if (!o.tc || (n->flags & DCNN_FLAG_HYBRID_DISPATCH)) {
-        TimeScope ts(n, st, DCNN_KCLASS_CONV);
-        launch_conv_cc(cp, n->dtype, n->cache32, o.grid_cc, st);
+        TimeScope ts(n, ost, DCNN_KCLASS_CONV);
+        launch_conv_cc(cp, n->dtype, n->cache32, o.grid_cc, ost);
         ++k;
       }
       if (o.tc) {
@@ -300,8 +342,8 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
         p.list = o.list_tc;
         p.count = n->counts + o.cnt_idx + 1;
         p.ep = make_epi(n, i);
-        TimeScope ts(n, st, DCNN_KCLASS_CONV);
-        launch_conv_tc(p, n->cache32, o.grid_tc, st);
+        TimeScope ts(n, ost, DCNN_KCLASS_CONV);
+        launch_conv_tc(p, n->cache32, o.grid_tc, ost);
         ++k;
       }
     } else {
@@ -323,16 +365,21 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       pp.G = group_lanes(o.C);
       pp.ep = make_epi(n, i);
       {
-        TimeScope ts(n, st, DCNN_KCLASS_POINTWISE);
-        launch_pointwise(pp, n->dtype, n->cache32, st);
+        TimeScope ts(n, ost, DCNN_KCLASS_POINTWISE);
+        launch_pointwise(pp, n->dtype, n->cache32, ost);
       }
       ++k;
       if (o.kind == DCNN_OP_MAXPOOL) {
-        TimeScope ts(n, st, DCNN_KCLASS_POINTWISE);
-        launch_pool_update(pp, n->dtype, n->cache32, st);
+        TimeScope ts(n, ost, DCNN_KCLASS_POINTWISE);
+        launch_pool_update(pp, n->dtype, n->cache32, ost);
         ++k;
       }
     }
+    if (NS) cudaEventRecord(n->ev_done[i], ost);
+  }
+  for (int k2 = 1; k2 <= NS; ++k2) {
+    cudaEventRecord(n->ev_join[k2 - 1], n->aux[k2 - 1]);
+    cudaStreamWaitEvent(st, n->ev_join[k2 - 1], 0);
   }
   launch_end_frame(n->first, n->frame_idx, n->S, st);
   ++k;
@@ -361,6 +408,11 @@ void dcnn_destroy_net(dcnn_net* n) {
   if (n->exec) cudaGraphExecDestroy(n->exec);
   if (n->graph) cudaGraphDestroy(n->graph);
   if (n->cap) cudaStreamDestroy(n->cap);
+  for (auto a : n->aux) cudaStreamDestroy(a);
+  for (auto e : n->ev_done) cudaEventDestroy(e);
+  for (auto e : n->ev_join) cudaEventDestroy(e);
+  if (n->ev_fork) cudaEventDestroy(n->ev_fork);
+  if (n->ev_input) cudaEventDestroy(n->ev_input);
   for (void* p : n->allocs) cudaFree(p);
   if (n->err_host) cudaFreeHost(n->err_host);
   for (auto& t : n->timed) {
@@ -610,6 +662,23 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   CUDA_TRY(conv_cc_init());
   CUDA_TRY(conv_tc_init());
   CUDA_TRY(cudaStreamCreateWithFlags(&n->cap, cudaStreamNonBlocking));
+  {
+    static const int nbranch = getenv("DCNN_BRANCH_STREAMS") ? atoi(getenv("DCNN_BRANCH_STREAMS")) : 3;
+    for (int k2 = 0; k2 < nbranch; ++k2) {
+      cudaStream_t a;
+      CUDA_TRY(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+      n->aux.push_back(a);
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      n->ev_join.push_back(e);
+    }
+    if (nbranch) {
+      CUDA_TRY(cudaEventCreateWithFlags(&n->ev_fork, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&n->ev_input, cudaEventDisableTiming));
+      n->ev_done.resize(L);
+      for (int i = 0; i < L; ++i) CUDA_TRY(cudaEventCreateWithFlags(&n->ev_done[i], cudaEventDisableTiming));
+    }
+  }
   CUDA_TRY(cudaDeviceSynchronize());
   return DCNN_OK;
 }

@@ -19,6 +19,8 @@ namespace dcnn {
 
 // ------------------------------------------------------------------ a2
 __global__ void __launch_bounds__(128) k_tiles(TileParams p) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int s_out, s_in;
   const int ntiles = p.S * p.nty * p.ntx;
   const int tid = threadIdx.x;
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(128) k_tiles(TileParams p) {
 void launch_tiles(const TileParams& p, cudaStream_t st) {
   const int ntiles = p.S * p.nty * p.ntx;
   const int grid = ntiles < 148 * 16 ? ntiles : 148 * 16;
-  k_tiles<<<grid, 128, 0, st>>>(p);
+  launch_k(k_tiles, dim3(grid), dim3(128), 0, st, 1, p);
 }
 
 // ------------------------------------------------------------------ a4
@@ -96,6 +98,8 @@ size_t conv_cc_smem(const ConvCCParams& p) {
 
 template <typename T, typename TC, int ACT>
 __global__ void __launch_bounds__(CC_THREADS) k_conv_cc(ConvCCParams p) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem[];
   float* win = reinterpret_cast<float*>(smem);
   uint8_t* wmask = smem + ((size_t)p.WH * p.WW * p.CIC * sizeof(float) + 15) / 16 * 16;
@@ -247,10 +251,10 @@ void launch_conv_cc(const ConvCCParams& p, int dtype, int cache32, int grid, cud
   act_dispatch(p.ep.act, [&](auto A) {
     constexpr int ACT = decltype(A)::value;
     if (dtype == 1) {
-      if (cache32) k_conv_cc<__half, float, ACT><<<grid, CC_THREADS, smem, st>>>(p);
-      else k_conv_cc<__half, __half, ACT><<<grid, CC_THREADS, smem, st>>>(p);
+      if (cache32) launch_k(k_conv_cc<__half, float, ACT>, dim3(grid), dim3(CC_THREADS), smem, st, 1, p);
+      else launch_k(k_conv_cc<__half, __half, ACT>, dim3(grid), dim3(CC_THREADS), smem, st, 1, p);
     } else {
-      k_conv_cc<float, float, ACT><<<grid, CC_THREADS, smem, st>>>(p);
+      launch_k(k_conv_cc<float, float, ACT>, dim3(grid), dim3(CC_THREADS), smem, st, 1, p);
     }
   });
 }

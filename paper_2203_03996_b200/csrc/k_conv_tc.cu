@@ -88,13 +88,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
 #ifdef DCNN_TRACE
   const unsigned long long t0 = gtime();
 #endif
-  const int count = *p.count;
+  pdl_trigger();
   // a cluster of nsplit CTAs shares each tile; CTA `rank` owns output channels
   // [rank*Ns, rank*Ns+Ns).  Clusters iterate the tile list persistently.
   const int nsplit = p.nsplit;
   const int rank = nsplit > 1 ? (int)tc::cluster_rank() : 0;
   const int cid = blockIdx.x / nsplit, ncl = gridDim.x / nsplit;
-  if (cid >= count) return;                   // uniform per cluster: no tile
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ntaps = p.kh * p.kw;
   const int ngroups = ntaps / p.tg;           // weight stages per channel block (tg taps each)
@@ -118,6 +117,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   TRACE(threadIdx.x == 0, 0, t0);
+  // everything above overlapped the previous kernel (PDL); its outputs are needed now
+  pdl_wait();
+  const int count = *p.count;
+  if (cid < count) {                          // uniform per cluster
 
   if (warp >= 4 && warp < 8) {
     // ---------------------------------------------------------------- halo loaders
@@ -400,6 +403,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
     unsigned n = (unsigned)warp_sum((int)nact);
     warp_count_flush(e.n_active, lane, n);
   }
+  }
   if (nsplit > 1) tc::cluster_sync_all();     // partners may still read our smem
   else __syncthreads();
 #ifdef DCNN_TRACE
@@ -443,22 +447,16 @@ cudaError_t conv_tc_init() {
 }
 
 void launch_conv_tc(const ConvTCParams& p, int cache32, int grid, cudaStream_t st) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = conv_tc_smem(p);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = p.nsplit;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
   act_dispatch(p.ep.act, [&](auto A) {
     constexpr int ACT = decltype(A)::value;
-    if (cache32) cudaLaunchKernelEx(&cfg, k_conv_tc<float, ACT>, p);
-    else cudaLaunchKernelEx(&cfg, k_conv_tc<__half, ACT>, p);
+    // at least 116 KB of shared memory: never two tensor-core CTAs on one SM, so each owns
+    // the SM's TMEM outright even when branch streams run several conv kernels at once (two
+    // co-resident CTAs each holding TMEM while waiting for a cluster partner could deadlock)
+    const size_t smem = conv_tc_smem(p) > 116 * 1024 ? conv_tc_smem(p) : 116 * 1024;
+    // nsplit > 1: launched as clusters of nsplit CTAs (the kernel only uses cluster
+    // barriers / DSMEM in that case)
+    if (cache32) launch_k(k_conv_tc<float, ACT>, dim3(grid), dim3(TC_THREADS), smem, st, p.nsplit, p);
+    else launch_k(k_conv_tc<__half, ACT>, dim3(grid), dim3(TC_THREADS), smem, st, p.nsplit, p);
   });
 }
 

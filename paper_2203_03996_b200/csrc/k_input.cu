@@ -19,6 +19,8 @@ constexpr int IN_RMAX = 16;
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_input(InputParams p) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ uint8_t m0[(IN_TS + 2 * IN_RMAX) * (IN_TS + 2 * IN_RMAX)];
   __shared__ uint8_t m1[(IN_TS + 2 * IN_RMAX) * IN_TS];
   const int tiles_x = (p.W + IN_TS - 1) / IN_TS;
@@ -103,12 +105,14 @@ __global__ void __launch_bounds__(256) k_input(InputParams p) {
 void launch_input(const InputParams& p, int dtype, cudaStream_t st) {
   const int tiles = p.S * ((p.H + IN_TS - 1) / IN_TS) * ((p.W + IN_TS - 1) / IN_TS);
   const int grid = tiles < 148 * 8 ? tiles : 148 * 8;
-  if (dtype == 1) k_input<__half><<<grid, 256, 0, st>>>(p);
-  else k_input<float><<<grid, 256, 0, st>>>(p);
+  if (dtype == 1) launch_k(k_input<__half>, dim3(grid), dim3(256), 0, st, 1, p);
+  else launch_k(k_input<float>, dim3(grid), dim3(256), 0, st, 1, p);
 }
 
 // Clears the first-frame flags after the frame and advances frame counters.
 __global__ void k_end_frame(uint8_t* first, long long* frame_idx, int S) {
+  pdl_trigger();
+  pdl_wait();
   for (int s = threadIdx.x; s < S; s += blockDim.x) {
     first[s] = 0;
     frame_idx[s] += 1;
@@ -116,7 +120,7 @@ __global__ void k_end_frame(uint8_t* first, long long* frame_idx, int S) {
 }
 
 void launch_end_frame(uint8_t* first, long long* frame_idx, int S, cudaStream_t st) {
-  k_end_frame<<<1, 128, 0, st>>>(first, frame_idx, S);
+  launch_k(k_end_frame, dim3(1), dim3(128), 0, st, 1, first, frame_idx, S);
 }
 
 }  // namespace dcnn

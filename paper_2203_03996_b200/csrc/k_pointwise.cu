@@ -181,6 +181,8 @@ __device__ __forceinline__ float pw_scalar(const PwParams& p, long long pix, int
 
 template <typename T, typename TC, int KIND, int ACT>
 __global__ void __launch_bounds__(256) k_pointwise(PwParams p) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const long long npix = (long long)p.S * p.H * p.W;
   const long long HWo = (long long)p.H * p.W;
@@ -222,6 +224,8 @@ __global__ void __launch_bounds__(256) k_pointwise(PwParams p) {
 // One thread per (pixel, channel) element; coalesced over channels.
 template <typename T, typename TC>
 __global__ void __launch_bounds__(256) k_pool_update(PwParams p) {
+  pdl_trigger();
+  pdl_wait();
   const int C = p.ep.C;
   const long long HWi = (long long)p.Hi * p.Wi;
   const long long n = (long long)p.S * HWi * C;
@@ -246,16 +250,16 @@ static void pw_dispatch(const PwParams& p, cudaStream_t st) {
   const int grid = pw_grid(((long long)p.S * p.H * p.W + ppw - 1) / ppw, 8);
   switch (p.kind) {
     case K_ACT:
-      act_dispatch(p.ep.act, [&](auto a) { k_pointwise<T, TC, K_ACT, decltype(a)::value><<<grid, 256, 0, st>>>(p); });
+      act_dispatch(p.ep.act, [&](auto a) { launch_k(k_pointwise<T, TC, K_ACT, decltype(a)::value>, dim3(grid), dim3(256), 0, st, 1, p); });
       break;
     case K_ADD:
-      act_dispatch(p.ep.act, [&](auto a) { k_pointwise<T, TC, K_ADD, decltype(a)::value><<<grid, 256, 0, st>>>(p); });
+      act_dispatch(p.ep.act, [&](auto a) { launch_k(k_pointwise<T, TC, K_ADD, decltype(a)::value>, dim3(grid), dim3(256), 0, st, 1, p); });
       break;
-    case K_MAXPOOL: k_pointwise<T, TC, K_MAXPOOL, ACT_NONE><<<grid, 256, 0, st>>>(p); break;
-    case K_AVGPOOL: k_pointwise<T, TC, K_AVGPOOL, ACT_NONE><<<grid, 256, 0, st>>>(p); break;
-    case K_UP: k_pointwise<T, TC, K_UP, ACT_NONE><<<grid, 256, 0, st>>>(p); break;
-    case K_CONCAT: k_pointwise<T, TC, K_CONCAT, ACT_NONE><<<grid, 256, 0, st>>>(p); break;
-    case K_AFFINE: k_pointwise<T, TC, K_AFFINE, ACT_NONE><<<grid, 256, 0, st>>>(p); break;
+    case K_MAXPOOL: launch_k(k_pointwise<T, TC, K_MAXPOOL, ACT_NONE>, dim3(grid), dim3(256), 0, st, 1, p); break;
+    case K_AVGPOOL: launch_k(k_pointwise<T, TC, K_AVGPOOL, ACT_NONE>, dim3(grid), dim3(256), 0, st, 1, p); break;
+    case K_UP: launch_k(k_pointwise<T, TC, K_UP, ACT_NONE>, dim3(grid), dim3(256), 0, st, 1, p); break;
+    case K_CONCAT: launch_k(k_pointwise<T, TC, K_CONCAT, ACT_NONE>, dim3(grid), dim3(256), 0, st, 1, p); break;
+    case K_AFFINE: launch_k(k_pointwise<T, TC, K_AFFINE, ACT_NONE>, dim3(grid), dim3(256), 0, st, 1, p); break;
   }
 }
 
@@ -271,10 +275,10 @@ void launch_pointwise(const PwParams& p, int dtype, int cache32, cudaStream_t st
 void launch_pool_update(const PwParams& p, int dtype, int cache32, cudaStream_t st) {
   const int grid = pw_grid((long long)p.S * p.Hi * p.Wi * p.ep.C, 256 * 4);
   if (dtype == 1) {
-    if (cache32) k_pool_update<__half, float><<<grid, 256, 0, st>>>(p);
-    else k_pool_update<__half, __half><<<grid, 256, 0, st>>>(p);
+    if (cache32) launch_k(k_pool_update<__half, float>, dim3(grid), dim3(256), 0, st, 1, p);
+    else launch_k(k_pool_update<__half, __half>, dim3(grid), dim3(256), 0, st, 1, p);
   } else {
-    k_pool_update<float, float><<<grid, 256, 0, st>>>(p);
+    launch_k(k_pool_update<float, float>, dim3(grid), dim3(256), 0, st, 1, p);
   }
 }
 
