@@ -313,11 +313,12 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       tp.list_cc = o.list_cc; tp.count_cc = n->counts + o.cnt_idx;
       tp.list_tc = o.list_tc; tp.count_tc = n->counts + o.cnt_idx + 1;
       tp.stats = n->stats + (size_t)(i + 1) * 8;
-      {
+      const bool fused = o.tc && !(n->flags & DCNN_FLAG_HYBRID_DISPATCH);
+      if (!fused) {                    // tensor-core convs decide their tiles in-kernel
         TimeScope ts(n, ost, DCNN_KCLASS_TILES);
         launch_tiles(tp, ost);
+        ++k;
       }
-      ++k;
       ConvCCParams cp;
       cp.S = n->S; cp.H = o.Hi; cp.W = o.Wi; cp.Ci = o.Ci;
       cp.Ho = o.H; cp.Wo = o.W; cp.Co = o.C; cp.Cp = o.Cp;
@@ -341,6 +342,9 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
         p.mask_in = src_mask(o.in[0]);
         p.list = o.list_tc;
         p.count = n->counts + o.cnt_idx + 1;
+        p.fused = fused ? 1 : 0;
+        p.ntiles = n->S * o.nty * o.ntx;
+        p.tstats = n->stats + (size_t)(i + 1) * 8;
         p.ep = make_epi(n, i);
         TimeScope ts(n, ost, DCNN_KCLASS_CONV);
         launch_conv_tc(p, n->cache32, o.grid_tc, ost);
@@ -663,7 +667,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   CUDA_TRY(conv_tc_init());
   CUDA_TRY(cudaStreamCreateWithFlags(&n->cap, cudaStreamNonBlocking));
   {
-    static const int nbranch = getenv("DCNN_BRANCH_STREAMS") ? atoi(getenv("DCNN_BRANCH_STREAMS")) : 3;
+    static const int nbranch = getenv("DCNN_BRANCH_STREAMS") ? atoi(getenv("DCNN_BRANCH_STREAMS")) : 5;
     for (int k2 = 0; k2 < nbranch; ++k2) {
       cudaStream_t a;
       CUDA_TRY(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));

@@ -44,7 +44,14 @@ __shared__ unsigned long long g_tr[80];
 #endif
 
 struct TcSmem {                 // byte offsets inside dynamic shared memory
-  uint32_t bar, tmem_slot, pmax, hmask, a0, a1, b0;
+  uint32_t bar, tmem_slot, info, pmax, hmask, a0, a1, b0;
+};
+
+// per-tile decision published by the halo loaders (a2 fused into a3): whether any output
+// pixel of the tile is active, and the 128 receptive-field-OR bits (m_conv, Z7)
+struct TileInfo {
+  int active;
+  uint32_t bits[4];
 };
 
 constexpr int TC_HMASK_BYTES = 1024;   // halo update mask of the current tile (u8)
@@ -53,6 +60,7 @@ __host__ __device__ inline TcSmem tc_layout(const ConvTCParams& p) {
   TcSmem L;
   L.bar = 0;                                  // up to 32 mbarriers
   L.tmem_slot = 32 * 8;
+  L.info = 264;                               // [2] TileInfo (40 B)
   L.pmax = 384;                               // [2][128] f32 partial max-norms (cluster exchange)
   L.hmask = L.pmax + 1024;
   L.a0 = L.hmask + TC_HMASK_BYTES;
@@ -79,6 +87,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
   uint64_t* acc_full = bars + 20;             // [2]
   uint64_t* acc_empty = bars + 22;            // [2]
   uint64_t* xch = bars + 24;                  // [2] cluster max-norm exchange
+  uint64_t* info_full = bars + 26;            // [2] tile decision published
+  uint64_t* info_empty = bars + 28;           // [2] tile decision consumed by all roles
+  TileInfo* info = reinterpret_cast<TileInfo*>(smem + L.info);
   float* pmax = reinterpret_cast<float*>(smem + L.pmax);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
   uint8_t* hmask = smem + L.hmask;
@@ -107,6 +118,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
       tc::mbar_init(&acc_full[i], 1);
       tc::mbar_init(&acc_empty[i], 128);
       tc::mbar_init(&xch[i], nsplit);
+      tc::mbar_init(&info_full[i], 1);
+      tc::mbar_init(&info_empty[i], 128 + 2);   // epilogue threads + producer + MMA
     }
     tc::mbar_fence_init();
   }
@@ -119,7 +132,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
   TRACE(threadIdx.x == 0, 0, t0);
   // everything above overlapped the previous kernel (PDL); its outputs are needed now
   pdl_wait();
-  const int count = *p.count;
+  // fused: every tile of the layer, statically strided over clusters; else the a2 list
+  const int count = p.fused ? p.ntiles : *p.count;
+  auto tile_of = [&](int ti) { return p.fused ? ti : p.list[ti]; };
   if (cid < count) {                          // uniform per cluster
 
   if (warp >= 4 && warp < 8) {
@@ -133,8 +148,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
     const int items = npx * nch;
     const int WQ = p.WWp / p.stride;
     int q = 0;                                 // global c-block counter (buffer ring)
-    for (int ti = cid; ti < count; ti += ncl) {
-      const int tile = p.list[ti];
+    int v = 0;                                 // tile counter (decision ring)
+    unsigned long long n_tot = 0, n_skip = 0, n_dense = 0, n_mc = 0;
+    for (int ti = cid; ti < count; ti += ncl, ++v) {
+      const int tile = tile_of(ti);
       const int s = tile / (p.nty * p.ntx);
       const int ty = (tile / p.ntx) % p.nty, tx = tile % p.ntx;
       const int iy0 = ty * 16 * p.stride - p.pad, ix0 = tx * 8 * p.stride - p.pad;
@@ -146,6 +163,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
       }
       tc::named_bar_sync(1, 128);
       TRACE(lt == 0 && ti == cid, 1, t0);
+      // a2 inside the conv: output pixel m = lt of the tile is active iff
+      // an input pixel of its receptive field is (Z7); the tile is skipped iff none is
+      const int r = lt >> 3, c = lt & 7;
+      const int oy = ty * 16 + r, ox = tx * 8 + c;
+      bool mc = false;
+      if (oy < p.Ho && ox < p.Wo)
+        for (int ky = 0; ky < p.kh; ++ky)
+          for (int kx = 0; kx < p.kw; ++kx)
+            mc |= hmask[(r * p.stride + ky * p.dil) * p.WW + c * p.stride + kx * p.dil] != 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, mc);
+      const int slot = v & 1;
+      tc::mbar_wait(&info_empty[slot], ((v >> 1) & 1) ^ 1);
+      if (lane == 0) info[slot].bits[warp - 4] = bal;
+      tc::named_bar_sync(1, 128);
+      const bool active = (info[slot].bits[0] | info[slot].bits[1] | info[slot].bits[2] | info[slot].bits[3]) != 0;
+      if (lt == 0) {
+        info[slot].active = active ? 1 : 0;
+        tc::mbar_arrive(&info_full[slot]);
+        ++n_tot;
+        if (active) {
+          ++n_dense;
+          n_mc += __popc(info[slot].bits[0]) + __popc(info[slot].bits[1]) + __popc(info[slot].bits[2]) +
+                  __popc(info[slot].bits[3]);
+        } else {
+          ++n_skip;
+        }
+      }
+      if (!active) {
+        // "independent of whether a tile is skipped, we write the update mask"
+        if (oy < p.Ho && ox < p.Wo && rank == 0) p.ep.mask[((long long)s * p.Ho + oy) * p.Wo + ox] = 0;
+        continue;
+      }
       const __half* src0 = p.delta_in + (long long)s * p.H * p.W * p.Ci;
       for (int cb = 0; cb < p.ncb; ++cb, ++q) {
         const int b = q & 1;
@@ -166,12 +215,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
         TRACE(lt == 0 && ti == cid && cb == 0, 2, t0);
       }
     }
+    if (p.fused && lt == 0 && rank == 0 && p.tstats) {
+      atomicAdd(&p.tstats[2], n_tot);
+      atomicAdd(&p.tstats[3], n_skip);
+      atomicAdd(&p.tstats[5], n_dense);
+      atomicAdd(&p.tstats[6], n_mc);
+    }
   } else if (warp == 8) {
     // ---------------------------------------------------------------- weight producer
     // the whole warp runs the (warp-uniform) loop so the compiler keeps indices in
     // uniform registers; one elected lane issues the bulk copies
-    int j = 0;
-    for (int ti = cid; ti < count; ti += ncl) {
+    int j = 0, v = 0;
+    for (int ti = cid; ti < count; ti += ncl, ++v) {
+      tc::mbar_wait(&info_full[v & 1], (v >> 1) & 1);
+      const bool active = info[v & 1].active != 0;
+      __syncwarp();
+      if (tc::elect_one()) tc::mbar_arrive(&info_empty[v & 1]);
+      __syncwarp();
+      if (!active) continue;
       for (int st = 0; st < nsteps; ++st, ++j) {
         const int slot = j % p.stages;
         tc::mbar_wait(&b_empty[slot], ((j / p.stages) & 1) ^ 1);
@@ -196,8 +257,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
     const uint32_t lbo_b = (uint32_t)(p.Ns * 16);
     const int WQ = p.WWp / p.stride;
     const uint32_t idesc = tc::idesc_f16(128, p.Ns);
-    int j = 0, q = 0, u = 0;
-    for (int ti = cid; ti < count; ti += ncl, ++u) {
+    int j = 0, q = 0, u = 0, v = 0;
+    for (int ti = cid; ti < count; ti += ncl, ++v) {
+      tc::mbar_wait(&info_full[v & 1], (v >> 1) & 1);
+      const bool active = info[v & 1].active != 0;
+      __syncwarp();
+      if (tc::elect_one()) tc::mbar_arrive(&info_empty[v & 1]);
+      __syncwarp();
+      if (!active) continue;
       const int acc = u % p.n_acc;
       tc::mbar_wait(&acc_empty[acc], ((u / p.n_acc) & 1) ^ 1);
       tc::tc_fence_after();
@@ -240,6 +307,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
       if (tc::elect_one()) tc::mma_commit(&acc_full[acc]);  // accumulator ready for the epilogue
       __syncwarp();
       TRACE(ti == cid && lane == 0, 3, t0);
+      ++u;
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 0-3)
@@ -253,15 +321,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
     const float eps = *e.eps;
     const float* bias = p.bias + cb0;
     unsigned nact = 0;
-    int u = 0;
-    for (int ti = cid; ti < count; ti += ncl, ++u) {
-      const int tile = p.list[ti];
+    int u = 0, v = 0;
+    for (int ti = cid; ti < count; ti += ncl, ++v) {
+      tc::mbar_wait(&info_full[v & 1], (v >> 1) & 1);
+      const bool tile_active = info[v & 1].active != 0;
+      const bool mcb = (info[v & 1].bits[tid >> 5] >> (tid & 31)) & 1u;   // m_conv of my pixel
+      tc::mbar_arrive(&info_empty[v & 1]);
+      if (!tile_active) continue;
+      const int tile = tile_of(ti);
       const int s = tile / (p.nty * p.ntx);
       const int ty = (tile / p.ntx) % p.nty, tx = tile % p.ntx;
       const int oy = ty * 16 + tid / 8, ox = tx * 8 + tid % 8;
       const bool inb = oy < p.Ho && ox < p.Wo;
       const long long pix = ((long long)s * p.Ho + oy) * p.Wo + ox;
-      const bool act = inb && e.mask[pix] != 0;      // m_conv written by a2
+      const bool act = inb && mcb;
       const bool first = e.first[s] != 0;
       const int acc = u % p.n_acc;
       tc::mbar_wait(&acc_full[acc], (u / p.n_acc) & 1);
@@ -394,10 +467,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(ConvTCParams p) {
         }
       }
       TRACE(tid == 0 && u == 0, 5, t0);
-      if (act && rank == 0) e.mask[pix] = upd ? 1 : 0;
+      if (inb && rank == 0) e.mask[pix] = upd ? 1 : 0;     // final mask of every tile pixel
       nact += (upd && rank == 0) ? 1 : 0;
       tc::tc_fence_before();
       tc::mbar_arrive(&acc_empty[acc]);
+      ++u;
     }
     // one atomic per warp
     unsigned n = (unsigned)warp_sum((int)nact);

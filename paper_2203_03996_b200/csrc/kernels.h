@@ -78,6 +78,9 @@ struct ConvTCParams {
   int tmem_cols;
   int nsplit, Ns;               // output channels split over a cluster of nsplit CTAs (Ns each)
   int dbg;                      // debug: bit0 skip weight copies, bit1 skip halo copies
+  int fused;                    // 1: iterate all tiles, decide activity in-kernel (no a2 launch)
+  int ntiles;                   // S*nty*ntx (fused mode)
+  unsigned long long* tstats;   // fused mode: [.., tiles_total, skip, sparse, dense, m_conv px]
   const __half* delta_in;
   const uint8_t* mask_in;
   const __half* wtc;            // [nsplit][ncb*kh*kw][BK/8][Ns][8] fp16 (smem image of each step)
