@@ -182,28 +182,31 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
   p.WWp = s * WQ;
   const size_t budget = 226 * 1024 - 384 - 1024 - 1024;
   const int ntaps = o.kh * o.kw;
-  // prefer wide K per weight stage (fewer mbarrier round trips), then more stages
-  for (int BK = 64; BK >= 16; BK /= 2) {
-    if (o.Ci % BK) continue;
-    const int plane = (p.HH * p.WWp * 16 + 127) / 128 * 128 + 16;
-    const int a_bytes = ((BK / 8) * plane + 127) / 128 * 128;
-    if ((p.stride * p.WWp * 16) >> 4 >= (1 << 14) || plane >> 4 >= (1 << 14)) continue;
-    for (int tg = ntaps; tg >= 1; --tg) {
-      if (ntaps % tg) continue;
-      const int b_bytes = tg * p.Ns * BK * 2;
-      if (2 * (size_t)a_bytes + 2 * (size_t)b_bytes > budget) continue;
-      int stages = (int)((budget - 2 * (size_t)a_bytes) / b_bytes);
-      if (stages > 8) stages = 8;
-      p.BK = BK;
-      p.ncb = o.Ci / BK;
-      p.plane = plane;
-      p.a_bytes = a_bytes;
-      p.b_bytes = b_bytes;
-      p.stages = stages;
-      p.tg = tg;
-      return true;
+  // prefer wide K per weight stage (fewer mbarrier round trips) while keeping >= 4 stages
+  // in flight (weights stream from L2 while the MMAs of earlier stages run); fall back to
+  // fewer stages only when nothing else fits
+  for (int min_stages = 4; min_stages >= 2; min_stages -= 2)
+    for (int BK = 64; BK >= 16; BK /= 2) {
+      if (o.Ci % BK) continue;
+      const int plane = (p.HH * p.WWp * 16 + 127) / 128 * 128 + 16;
+      const int a_bytes = ((BK / 8) * plane + 127) / 128 * 128;
+      if ((p.stride * p.WWp * 16) >> 4 >= (1 << 14) || plane >> 4 >= (1 << 14)) continue;
+      for (int tg = ntaps; tg >= 1; --tg) {
+        if (ntaps % tg) continue;
+        const int b_bytes = tg * p.Ns * BK * 2;
+        if (2 * (size_t)a_bytes + (size_t)min_stages * b_bytes > budget) continue;
+        int stages = (int)((budget - 2 * (size_t)a_bytes) / b_bytes);
+        if (stages > 8) stages = 8;
+        p.BK = BK;
+        p.ncb = o.Ci / BK;
+        p.plane = plane;
+        p.a_bytes = a_bytes;
+        p.b_bytes = b_bytes;
+        p.stages = stages;
+        p.tg = tg;
+        return true;
+      }
     }
-  }
   return false;
 }
 
