@@ -200,6 +200,17 @@ DCNN_API dcnn_status dcnn_kernel_timing(dcnn_net* net, int32_t kernel_class, flo
  * that any read of a masked-off (stale) value would surface in the outputs. */
 DCNN_API dcnn_status dcnn_debug_poison(dcnn_net* net);
 
+/* Debug timeline of the tensor-core conv kernel: when a net is created with the
+ * environment variable DCNN_TC_DBG=4, CTA 0 of every tcgen05 conv launch writes
+ * %globaltimer stamps (ns) of its pipeline milestones into a process-wide table of
+ * 32 slots; this copies the table (of the latest launch) to host32[32].  Syncs the
+ * device.  Slots: 0 start, 1 setup done, 2 after the PDL wait, 3 first halo mask
+ * staged, 4 first tile published, 5 first halo group issued, 6 loaders done,
+ * 7 first halo landed (MMA), 8 first weight step landed, 9 first tile's MMAs
+ * committed, 10/11 epilogue before/after the first accumulator wait, 12 first
+ * tile written, 13 roles done, 14 after the final barrier. */
+DCNN_API dcnn_status dcnn_debug_tc_trace(uint64_t* host32);
+
 /* Number of kernel launches enqueued by one process_frame (graph nodes). */
 DCNN_API int32_t dcnn_kernels_per_frame(dcnn_net* net);
 

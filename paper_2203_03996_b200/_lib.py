@@ -81,10 +81,11 @@ def load_library(path: str = LIB_PATH):
     lib.dcnn_enable_kernel_timing.argtypes = [vp, C.c_int32]
     lib.dcnn_kernel_timing.argtypes = [vp, C.c_int32, C.POINTER(C.c_float), C.POINTER(C.c_int32)]
     lib.dcnn_debug_poison.argtypes = [vp]
+    lib.dcnn_debug_tc_trace.argtypes = [vp]
     for name in ["dcnn_create_net", "dcnn_set_threshold", "dcnn_process_frame",
                  "dcnn_process_frame_host", "dcnn_reset", "dcnn_op_shape", "dcnn_get_stats",
                  "dcnn_debug_read", "dcnn_enable_kernel_timing", "dcnn_kernel_timing",
-                 "dcnn_debug_poison"]:
+                 "dcnn_debug_poison", "dcnn_debug_tc_trace"]:
         getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -103,6 +104,15 @@ def _check(lib, st):
 
 def _fptr(a):
     return a.ctypes.data_as(C.POINTER(C.c_float)) if a is not None else None
+
+
+def debug_tc_trace():
+    """Timeline (ns, %globaltimer) of CTA 0 of the latest tcgen05 conv launch; needs a net
+    created with DCNN_TC_DBG=4 in the environment (include/dcnn.h dcnn_debug_tc_trace)."""
+    lib = load_library()
+    buf = np.zeros(32, dtype=np.uint64)
+    _check(lib, lib.dcnn_debug_tc_trace(buf.ctypes.data))
+    return buf
 
 
 class DeltaNet:

@@ -3,6 +3,8 @@
 // create: validate + shape inference + weight copy/cast + device state + plan.
 // process_frame: one CUDA-graph launch per frame (captured on first use); every
 // per-layer work count lives on the device, so there is no host sync per frame.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -161,49 +163,87 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
   // split output channels over a cluster when the layer has few tiles (small maps,
   // wide layers): every CTA then streams only its slice of the weights
   const int ntiles = S * ((o.H + 15) / 16) * ((o.W + 7) / 8);
-  int ns = 1;
+  int ns0 = 1;
   static const int max_split = getenv("DCNN_TC_MAX_SPLIT") ? atoi(getenv("DCNN_TC_MAX_SPLIT")) : 8;
-  while (ns < max_split && p.Np % (16 * ns * 2) == 0 && p.Np / (ns * 2) >= 32 && ntiles * ns * 2 <= 2 * 148) ns *= 2;
-  while (p.Np / ns > 256) ns *= 2;            // one MMA N <= 256 per CTA
-  if (p.Np % (16 * ns)) return false;
-  p.nsplit = ns;
-  p.Ns = p.Np / ns;
+  while (ns0 < max_split && p.Np % (16 * ns0 * 2) == 0 && p.Np / (ns0 * 2) >= 32 && ntiles * ns0 * 2 <= 2 * 148) ns0 *= 2;
+  while (p.Np / ns0 > 256) ns0 *= 2;            // one MMA N <= 256 per CTA
+  if (p.Np % (16 * ns0)) return false;
   p.dbg = getenv("DCNN_TC_DBG") ? atoi(getenv("DCNN_TC_DBG")) : 0;
-  p.n_acc = 2;
-  p.acc_stride = (p.Ns + 31) / 32 * 32;
-  int tc = 32;
-  while (tc < 2 * p.acc_stride) tc *= 2;
-  p.tmem_cols = tc;
   const int s = o.stride, d = o.dil;
+  if (s > 2 || o.kh * o.kw > 64) return false;         // stride phases / tap table
   p.HH = 15 * s + (o.kh - 1) * d + 1;
   p.WW = 7 * s + (o.kw - 1) * d + 1;
-  if (p.HH * p.WW > 1024) return false;                 // halo mask staging buffer
-  const int WQ = (p.WW + s - 1) / s;
-  p.WWp = s * WQ;
-  const size_t budget = 226 * 1024 - 384 - 1024 - 1024;
+  if (p.HH * p.WW > 1024 || p.HH > 256) return false;   // halo mask staging buffer, TMA box
+  p.WQ = (p.WW + s - 1) / s;
+  // fixed part of the layout (barriers, tile ring, halo masks): see tc_layout()
+  const size_t budget = 226 * 1024 - 6144;
   const int ntaps = o.kh * o.kw;
-  // prefer wide K per weight stage (fewer mbarrier round trips) while keeping >= 4 stages
-  // in flight (weights stream from L2 while the MMAs of earlier stages run); fall back to
-  // fewer stages only when nothing else fits
+  // halo buffer = [stride phase][8-channel plane][halo row][column of the phase][8 ch];
+  // every plane is one TMA box (128-B aligned), its byte size is the A-operand LBO
+  auto a_bytes_of = [&](int BK) {
+    const int plane = (p.HH * p.WQ * 16 + 127) / 128 * 128;
+    const int phase = (BK / 8) * plane;
+    return std::make_pair(plane, s * phase);
+  };
+  auto set_common = [&](int ns, int BK, int tg, int stages, int nab, int resident) {
+    p.nsplit = ns;
+    p.Ns = p.Np / ns;
+    p.BK = BK;
+    p.ncb = o.Ci / BK;
+    auto pa = a_bytes_of(BK);
+    p.plane = pa.first;
+    p.phase_bytes = (BK / 8) * pa.first;
+    p.a_bytes = pa.second;
+    p.tg = tg;
+    p.b_bytes = tg * p.Ns * BK * 2;
+    p.stages = stages;
+    p.n_abuf = nab;
+    p.resident = resident;
+    p.n_acc = 2;
+    p.acc_stride = (p.Ns + 31) / 32 * 32;
+    int tc = 32;
+    while (tc < 2 * p.acc_stride) tc *= 2;
+    p.tmem_cols = tc;
+  };
+  static const bool no_resident = getenv("DCNN_TC_NO_RESIDENT") != nullptr;
+  // 1. resident weights: the CTA's whole weight slice sits in smem next to >= 2 halo
+  //    buffers (loaded once per kernel, before the PDL wait); allow up to 4x more
+  //    channel splitting than parallelism alone asks for to get there
+  for (int ns = ns0; !no_resident && ns <= 8 && ns <= 4 * ns0; ns *= 2) {
+    if (p.Np % (16 * ns) || p.Np / ns < 16) break;
+    const int Ns = p.Np / ns;
+    for (int BK = 64; BK >= 16; BK /= 2) {
+      if (o.Ci % BK) continue;
+      const auto pa = a_bytes_of(BK);
+      if (pa.first >> 4 >= (1 << 14)) continue;                       // LBO field
+      const size_t wbytes = (size_t)Ns * ntaps * o.Ci * 2;
+      if (2 * (size_t)pa.second + wbytes > budget) continue;
+      const int ncb = o.Ci / BK;
+      int tg = 0;
+      for (int t = ntaps; t >= 1; --t)
+        if (ntaps % t == 0 && ncb * (ntaps / t) <= 16) { tg = t; break; }
+      if (!tg) continue;
+      const int nab = 2 * (size_t)pa.second + wbytes + pa.second <= budget ? 3 : 2;
+      set_common(ns, BK, tg, ncb * (ntaps / tg), nab, 1);
+      return true;
+    }
+  }
+  // 2. streamed weights: prefer wide K per weight stage (fewer mbarrier round trips)
+  //    while keeping >= 4 stages in flight (weights stream from L2 while the MMAs of
+  //    earlier stages run); fall back to fewer stages only when nothing else fits
   for (int min_stages = 4; min_stages >= 2; min_stages -= 2)
     for (int BK = 64; BK >= 16; BK /= 2) {
       if (o.Ci % BK) continue;
-      const int plane = (p.HH * p.WWp * 16 + 127) / 128 * 128 + 16;
-      const int a_bytes = ((BK / 8) * plane + 127) / 128 * 128;
-      if ((p.stride * p.WWp * 16) >> 4 >= (1 << 14) || plane >> 4 >= (1 << 14)) continue;
+      const auto pa = a_bytes_of(BK);
+      if (pa.first >> 4 >= (1 << 14)) continue;                       // LBO field
+      const int Ns = p.Np / ns0;
       for (int tg = ntaps; tg >= 1; --tg) {
         if (ntaps % tg) continue;
-        const int b_bytes = tg * p.Ns * BK * 2;
-        if (2 * (size_t)a_bytes + (size_t)min_stages * b_bytes > budget) continue;
-        int stages = (int)((budget - 2 * (size_t)a_bytes) / b_bytes);
-        if (stages > 8) stages = 8;
-        p.BK = BK;
-        p.ncb = o.Ci / BK;
-        p.plane = plane;
-        p.a_bytes = a_bytes;
-        p.b_bytes = b_bytes;
-        p.stages = stages;
-        p.tg = tg;
+        const size_t b_bytes = (size_t)tg * Ns * BK * 2;
+        if (2 * (size_t)pa.second + (size_t)min_stages * b_bytes > budget) continue;
+        int stages = (int)((budget - 2 * (size_t)pa.second) / b_bytes);
+        if (stages > 16) stages = 16;
+        set_common(ns0, BK, tg, stages, 2, 0);
         return true;
       }
     }
@@ -655,6 +695,28 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         if ((r = dalloc(n, &o.wtc, w.size() * 2))) return r;
         CUDA_TRY(cudaMemcpy(o.wtc, w.data(), w.size() * 2, cudaMemcpyHostToDevice));
         p.wtc = o.wtc;
+        // TMA view of the input delta [S][Hi][Wi][Ci] fp16: dims (C, x, y, stream); a box is
+        // 8 channels x one stride phase of the halo columns x all halo rows
+        {
+          static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+          if (!encode) {
+            void* f = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+            if (!f || q != cudaDriverEntryPointSuccess) return fail(DCNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+          }
+          void* src = o.in[0] < 0 ? n->in_delta : n->ops[o.in[0]].delta;
+          const cuuint64_t gdim[4] = {(cuuint64_t)o.Ci, (cuuint64_t)o.Wi, (cuuint64_t)o.Hi, (cuuint64_t)n->S};
+          const cuuint64_t gstr[3] = {(cuuint64_t)o.Ci * 2, (cuuint64_t)o.Wi * o.Ci * 2,
+                                      (cuuint64_t)o.Hi * o.Wi * o.Ci * 2};
+          const cuuint32_t box[4] = {8, (cuuint32_t)(o.stride * p.WQ), (cuuint32_t)p.HH, 1};
+          const cuuint32_t es[4] = {1, (cuuint32_t)o.stride, 1, 1};
+          CUresult cr = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, src, gdim, gstr, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+          if (cr != CUDA_SUCCESS) return fail(DCNN_ERR_CUDA, "conv " + std::to_string(i) + ": tensor map encode failed");
+        }
         const int ncl = std::max(1, std::min(n->S * o.nty * o.ntx, 148 / p.nsplit));
         o.grid_tc = ncl * p.nsplit;
       }
@@ -902,6 +964,13 @@ dcnn_status dcnn_debug_poison(dcnn_net* n) {
   for (auto& o : n->ops)
     CUDA_TRY(cudaMemset(o.delta, 0xFF, (size_t)n->S * o.H * o.W * o.C * es));
   CUDA_TRY(cudaDeviceSynchronize());
+  return DCNN_OK;
+}
+
+dcnn_status dcnn_debug_tc_trace(uint64_t* host32) {
+  if (!host32) return fail(DCNN_ERR_ARG, "null argument");
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(conv_tc_read_trace(reinterpret_cast<unsigned long long*>(host32)));
   return DCNN_OK;
 }
 

@@ -3,6 +3,7 @@
 // plan time and the amount of work is read from device memory, so one frame
 // is capturable as a single CUDA graph.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -65,19 +66,23 @@ cudaError_t conv_cc_init();     // once per process/device: raise the dynamic sm
 
 // ---------------------------------------------------------------- a3: tensor-core conv
 struct ConvTCParams {
+  CUtensorMap tmap;             // 4-D TMA view of the input delta (C, x, y, stream), box 8 ch
   int S, H, W, Ci;
   int Ho, Wo, Co, Np;           // Np: C_out padded to a multiple of 16
   int kh, kw, stride, pad, dil;
   int nty, ntx;                 // 16x8 output tiles
-  int HH, WW, WWp;              // halo rows, cols, padded cols (multiple of stride)
+  int HH, WW, WQ;               // halo rows, cols, cols per stride phase (ceil(WW / stride))
   int BK, ncb;                  // input channels per block, number of blocks
-  int plane;                    // bytes per 8-channel plane of the halo buffer (= LBO of A)
-  int a_bytes, b_bytes, stages; // halo buffer bytes, weight stage bytes, weight ring depth
+  int plane;                    // bytes of one 8-channel plane of one phase (= LBO of A)
+  int phase_bytes;              // bytes of one stride phase of a halo buffer (128-aligned)
+  int a_bytes, b_bytes, stages; // halo buffer bytes, weight step bytes, weight stages in smem
+  int n_abuf;                   // halo buffers (2..4)
+  int resident;                 // 1: all weight steps of the CTA stay in smem (stages = steps)
   int tg;                       // taps per weight stage (divides kh*kw)
   int n_acc, acc_stride;        // TMEM accumulators and their column stride
   int tmem_cols;
   int nsplit, Ns;               // output channels split over a cluster of nsplit CTAs (Ns each)
-  int dbg;                      // debug: bit0 skip weight copies, bit1 skip halo copies
+  int dbg;                      // debug: bit2 records the pipeline timeline of CTA 0
   int fused;                    // 1: iterate all tiles, decide activity in-kernel (no a2 launch)
   int ntiles;                   // S*nty*ntx (fused mode)
   unsigned long long* tstats;   // fused mode: [.., tiles_total, skip, sparse, dense, m_conv px]
@@ -91,6 +96,7 @@ struct ConvTCParams {
 size_t conv_tc_smem(const ConvTCParams& p);
 cudaError_t conv_tc_init();
 void launch_conv_tc(const ConvTCParams& p, int cache32, int grid, cudaStream_t st);
+cudaError_t conv_tc_read_trace(unsigned long long* host);   // debug timeline (dbg & 4)
 
 // ---------------------------------------------------------------- a6/a7 pointwise ops
 struct PwParams {

@@ -1,21 +1,26 @@
-"""Single-conv tensor-core kernel phase trace (needs libdcnn_trace.so built with -DDCNN_TRACE)."""
+"""Pipeline timeline of the tcgen05 conv (CTA 0) for single-conv nets: run with DCNN_TC_DBG=4."""
 import os, sys
-sys.path.insert(0, '.')
-os.environ["DCNN_LIB"] = os.path.abspath("paper_2203_03996_b200/libdcnn_trace.so")
+os.environ.setdefault("DCNN_TC_DBG", "4")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from synth import nets
 from paper_2203_03996_b200 import DeltaNet
-cfgs = [(64, 64, 64, 64, 3, "relu"), (128, 128, 64, 64, 3, "none"), (20, 20, 512, 512, 3, "silu")]
-for (H, W, ci, co, k, act) in cfgs:
+from paper_2203_03996_b200._lib import debug_tc_trace
+NAMES = ["start", "setup", "pdl_wait", "mask0", "pub0", "halo_iss0", "loaders_done", "halo_land0",
+         "w_land0", "mma0_commit", "epi_wait0", "epi_acc0", "epi_done0", "roles_done", "final_sync"]
+cfgs = [(16, 8, 64, 64, 3, 1), (128, 128, 64, 64, 3, 1), (20, 20, 512, 512, 3, 1), (160, 160, 64, 64, 3, 1)]
+for (H, W, ci, co, k, s) in cfgs:
     b = nets._Builder("c", H, W, ci, 0, "f16")
-    i = b.conv(-1, co, k, act=act)
+    i = b.conv(-1, co, k, stride=s, act="relu")
     b.net.outputs = [i]
     b.net.input_eps = -1.0
     eng = DeltaNet(b.net, 1)
-    x = torch.randn(1, H, W, ci, device="cuda").half()
-    out = [torch.empty((1,) + s, device="cuda") for s in eng.out_shapes]
-    print(f"=== conv {H}x{W} {ci}->{co} k{k} {act}", flush=True)
-    for t in range(3):
+    x = torch.randn(1, H, W, ci).half().cuda()
+    out = [torch.empty((1,) + sh, device="cuda") for sh in eng.out_shapes]
+    for t in range(4):
         eng.process_frame(x, out)
-        torch.cuda.synchronize()
+    tr = debug_tc_trace().astype(np.int64)
+    t0 = tr[0]
+    print(f"{H}x{W} {ci}->{co} k{k}s{s}: " + "  ".join(f"{n}={(tr[j] - t0) / 1e3:.2f}" for j, n in enumerate(NAMES)
+                                                     if tr[j]), flush=True)
     eng.close()
