@@ -165,6 +165,8 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
   const int ntiles = S * ((o.H + 15) / 16) * ((o.W + 7) / 8);
   int ns0 = 1;
   static const int max_split = getenv("DCNN_TC_MAX_SPLIT") ? atoi(getenv("DCNN_TC_MAX_SPLIT")) : 8;
+  // (down to N = 32 per CTA: a narrower slice shortens the epilogue of a tile, which is
+  // what bounds a layer with few tiles)
   while (ns0 < max_split && p.Np % (16 * ns0 * 2) == 0 && p.Np / (ns0 * 2) >= 32 && ntiles * ns0 * 2 <= 2 * 148) ns0 *= 2;
   while (p.Np / ns0 > 256) ns0 *= 2;            // one MMA N <= 256 per CTA
   if (p.Np % (16 * ns0)) return false;
@@ -173,10 +175,10 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
   if (s > 2 || o.kh * o.kw > 64) return false;         // stride phases / tap table
   p.HH = 15 * s + (o.kh - 1) * d + 1;
   p.WW = 7 * s + (o.kw - 1) * d + 1;
-  if (p.HH * p.WW > 1024 || p.HH > 256) return false;   // halo mask staging buffer, TMA box
+  if (p.HH * p.WW > 1024 || p.HH > 64 || p.WW > 32) return false;   // halo mask buffer, row bit masks
   p.WQ = (p.WW + s - 1) / s;
   // fixed part of the layout (barriers, tile ring, halo masks): see tc_layout()
-  const size_t budget = 226 * 1024 - 6144;
+  const size_t budget = 226 * 1024 - 69632;
   const int ntaps = o.kh * o.kw;
   // halo buffer = [stride phase][8-channel plane][halo row][column of the phase][8 ch];
   // every plane is one TMA box (128-B aligned), its byte size is the A-operand LBO

@@ -23,12 +23,13 @@
 // otherwise it streams through a ring of stages.  The accumulator lives in TMEM
 // (double-buffered) so the epilogue of tile t overlaps the MMAs of tile t+1.
 //
-// Warp roles (384 threads):
-//   warps 0-3   epilogue (TMEM lane quadrant = warp; thread = output pixel)
-//   warps 4-7   halo loaders (one elected lane issues the TMA copies; all zero inactive pixels)
-//   warp 8      weight producer (cp.async.bulk)
-//   warp 9      TMEM allocator + MMA issuer (one elected lane)
-//   warps 10-11 scouts: a2 fused into a3 -- stage the halo update mask of the next
+// Warp roles (384 threads = 3 warps per SM sub-partition, 168 registers):
+//   warps 0-7   epilogue: TMEM lane quadrant = warp % 4, thread = output pixel; warps 0-3
+//               own the first half of the output channels, warps 4-7 the second half
+//   warp 8      halo loader (one elected lane issues the TMA copies; all zero inactive pixels)
+//   warp 9      weight producer (cp.async.bulk)
+//   warp 10     TMEM allocator + MMA issuer (one elected lane)
+//   warp 11     scout: a2 fused into a3 -- stage the halo update mask of the next
 //               tiles, derive the receptive-field OR mask m_conv (Z7) and skip empty
 //               tiles ("before loading any other data, we first check the update
 //               mask"); only active tiles enter the pipeline, through
@@ -41,6 +42,7 @@ namespace dcnn {
 constexpr int TC_THREADS = 384;
 constexpr int TC_NI = 4;              // tile-slot ring depth (scouts run ahead by up to 4 tiles)
 constexpr int TC_HMASK_BYTES = 1024;  // halo update mask of one tile (u8)
+constexpr int TC_STAGE_WARP = 3 * 32 * 80;  // per-epilogue-warp row staging: 3 areas x 32 px x (64 + 16) B
 
 struct TileInfo {                     // one active tile published by the scouts
   int tile;                           // -1 terminates the ring
@@ -49,7 +51,7 @@ struct TileInfo {                     // one active tile published by the scouts
 };
 
 struct TcSmem {                       // byte offsets inside dynamic shared memory
-  uint32_t bar, tmem_slot, info, tapoff, pmax, hmask, a0, b0;
+  uint32_t bar, tmem_slot, info, tapoff, pmax, pm2, hmask, stage, a0, b0;
 };
 
 __host__ __device__ inline TcSmem tc_layout(const ConvTCParams& p) {
@@ -58,9 +60,11 @@ __host__ __device__ inline TcSmem tc_layout(const ConvTCParams& p) {
   L.tmem_slot = 512;
   L.info = 576;                       // [TC_NI] TileInfo (128 B)
   L.tapoff = 768;                     // [64] u32 A-operand byte offset of every tap
-  L.pmax = 1024;                      // [2][128] f32 partial max-norms (cluster exchange)
-  L.hmask = 2048;                     // [TC_NI][1024] u8
-  L.a0 = L.hmask + TC_NI * TC_HMASK_BYTES;
+  L.pmax = 1024;                      // [2][128] f32 per-CTA max-norms (cluster exchange)
+  L.pm2 = 2048;                       // [2][2][128] f32 per-half max-norms
+  L.hmask = 4096;                     // [TC_NI][1024] u8
+  L.stage = L.hmask + TC_NI * TC_HMASK_BYTES;   // [8 warps] row staging
+  L.a0 = L.stage + 8 * TC_STAGE_WARP;
   L.b0 = L.a0 + p.n_abuf * p.a_bytes;
   return L;
 }
@@ -92,6 +96,18 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// two floats <-> one packed f16x2 register (RNE), without addressable __half2 objects
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  uint32_t u;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(u) : "f"(hi), "f"(lo));
+  return u;
+}
+__device__ __forceinline__ float2 unpack_h2(uint32_t u) {
+  unsigned short lo, hi;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(u));
+  return make_float2(__half2float(__ushort_as_half(lo)), __half2float(__ushort_as_half(hi)));
 }
 
 // raw 16-B loads of cache rows (kept packed in registers until the accumulator lands)
@@ -145,23 +161,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   if (tid == 0) {
     for (int i = 0; i < 16; ++i) { tc::mbar_init(&b_full[i], 1); tc::mbar_init(&b_empty[i], 1); }
     for (int i = 0; i < 4; ++i) {
-      tc::mbar_init(&a_full[i], 128);
+      tc::mbar_init(&a_full[i], 32);
       tc::mbar_init(&a_empty[i], 1);
       tc::mbar_init(&a_tma[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&acc_full[i], 1);
-      tc::mbar_init(&acc_empty[i], 128);
+      tc::mbar_init(&acc_empty[i], 256);
       tc::mbar_init(&xch[i], nsplit);
     }
     for (int i = 0; i < TC_NI; ++i) {
       tc::mbar_init(&info_full[i], 1);
-      tc::mbar_init(&info_empty[i], 128 + 128 + 1 + 1);   // loaders + epilogue + MMA + producer
+      tc::mbar_init(&info_empty[i], 32 + 256 + 1 + 1);    // loader + epilogue + MMA + producer
     }
     tc::mbar_fence_init();
   }
-  if (warp == 9) tc::tmem_alloc(tmem_slot, p.tmem_cols);
-  if (warp == 8) {
+  if (warp == 10) tc::tmem_alloc(tmem_slot, p.tmem_cols);
+  if (warp == 9) {
     // A-operand start offset of every tap inside a halo buffer: phase (kx*d) mod s,
     // row ky*d, column of the phase (kx*d) div s
     for (int t = lane; t < ntaps; t += 32) {
@@ -180,7 +196,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   // weights are constant: start moving them before waiting on the producing kernel
   const unsigned char* wsrc = reinterpret_cast<const unsigned char*>(p.wtc) + (size_t)rank * nsteps * p.b_bytes;
   const int npre = p.resident ? nsteps : (p.stages < nsteps ? p.stages : nsteps);
-  if (warp == 8) {
+  if (warp == 9) {
     if (tc::elect_one()) {
       for (int st = 0; st < npre; ++st) {
         tc::mbar_arrive_expect_tx(&b_full[st], p.b_bytes);
@@ -195,11 +211,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   const int count = p.fused ? p.ntiles : *p.count;
   auto tile_of = [&](int ti) { return p.fused ? ti : p.list[ti]; };
 
-  if (warp >= 10) {
-    // ---------------------------------------------------------------- scouts
-    const int lt = tid - 320;                 // 0..63
+  if (warp == 11) {
+    // ---------------------------------------------------------------- scout (one warp)
+    // stages the tile's halo update mask (u8, for the loader's zero pass), packs each halo
+    // row into a bit mask, and ORs the rows/columns of every output pixel's receptive field
+    // (m_conv, Z7) with shifts; empty tiles are skipped here, before any data is loaded.
     const int npx = p.HH * p.WW;
-    const int hy_0 = lt / p.WW, hx_0 = lt - hy_0 * p.WW, dy64 = 64 / p.WW, dx64 = 64 - dy64 * p.WW;
+    const int hy_0 = lane / p.WW, hx_0 = lane - hy_0 * p.WW, dy32 = 32 / p.WW, dx32 = 32 - dy32 * p.WW;
+    uint32_t kxmask = 0;                       // column offsets of the taps
+    for (int kx = 0; kx < p.kw; ++kx) kxmask |= 1u << (kx * p.dil);
     unsigned long long n_tot = 0, n_skip = 0, n_dense = 0, n_mc = 0;
     int v = 0;
     bool own = false;                          // slot v % NI acquired
@@ -212,47 +232,61 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       const int ty = (tile / p.ntx) % p.nty, tx = tile % p.ntx;
       const int iy0 = ty * 16 * p.stride - p.pad, ix0 = tx * 8 * p.stride - p.pad;
       const uint8_t* mi = p.mask_in + (long long)s * p.H * p.W;
-      tc::named_bar_sync(3, 64);               // previous use of hm / info bits finished
+      __syncwarp();                            // previous use of hm / info bits finished
       {
-        int hy = hy_0, hx = hx_0;                // (hy, hx) of px = lt, advanced incrementally
-        for (int px = lt; px < npx; px += 64) {
+        int hy = hy_0, hx = hx_0;              // (hy, hx) of px = lane, advanced incrementally
+        for (int px = lane; px < npx; px += 32) {
           const int iy = iy0 + hy, ix = ix0 + hx;
           hm[px] = (iy >= 0 && iy < p.H && ix >= 0 && ix < p.W) ? mi[iy * p.W + ix] : 0;
-          hx += dx64;
-          hy += dy64;
+          hx += dx32;
+          hy += dy32;
           if (hx >= p.WW) { hx -= p.WW; ++hy; }
         }
       }
-      tc::named_bar_sync(3, 64);
-      TCTR(lt == 0 && ti == cid, 3);
-      // m_conv: output pixel m of the tile is active iff an input of its receptive field is
-      bool mc[2];
+      __syncwarp();
+      TCTR(lane == 0 && ti == cid, 3);
+      // halo row bit masks (bit hx of row hy), rows lane and lane + 32
+      uint32_t rb0 = 0, rb1 = 0;
+      if (lane < p.HH)
+        for (int hx = 0; hx < p.WW; ++hx) rb0 |= (uint32_t)(hm[lane * p.WW + hx] != 0) << hx;
+      if (lane + 32 < p.HH)
+        for (int hx = 0; hx < p.WW; ++hx) rb1 |= (uint32_t)(hm[(lane + 32) * p.WW + hx] != 0) << hx;
+      // output row r (lanes 0-15): OR of the rows r*s + ky*d, dilated by the tap columns,
+      // then every s-th bit = output columns 0..7
+      uint32_t rowbits = 0;
+      {
+        const int r = lane & 15;
+        uint32_t acc = 0;
+        for (int ky = 0; ky < p.kh; ++ky) {
+          const int hr = r * p.stride + ky * p.dil;
+          const uint32_t b0 = __shfl_sync(0xffffffffu, rb0, hr & 31);
+          const uint32_t b1 = __shfl_sync(0xffffffffu, rb1, hr & 31);
+          acc |= hr < 32 ? b0 : b1;
+        }
+        uint32_t dil = 0;                      // bit x set iff a tap column of x is active
+        for (uint32_t km = kxmask, o = 0; km; km >>= 1, ++o)
+          if (km & 1u) dil |= acc >> o;
+        for (int c = 0; c < 8; ++c) rowbits |= ((dil >> (c * p.stride)) & 1u) << c;
+        const int oy = ty * 16 + r;
+        if (oy >= p.Ho) rowbits = 0;
+        const int ncol = p.Wo - tx * 8;
+        if (ncol < 8) rowbits &= (1u << (ncol > 0 ? ncol : 0)) - 1u;
+      }
+      // pixel m = 8 r + c -> bit m & 31 of word m >> 5 (rows 4w .. 4w+3)
+      uint32_t w[4];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int m = lane + 64 * k + 32 * (warp - 10);
-        const int r = m >> 3, c = m & 7;
-        const int oy = ty * 16 + r, ox = tx * 8 + c;
-        bool a = false;
-        if (oy < p.Ho && ox < p.Wo)
-          for (int ky = 0; ky < p.kh; ++ky)
-            for (int kx = 0; kx < p.kw; ++kx)
-              a |= hm[(r * p.stride + ky * p.dil) * p.WW + c * p.stride + kx * p.dil] != 0;
-        mc[k] = a;
+      for (int q = 0; q < 4; ++q) {
+        uint32_t x = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x |= __shfl_sync(0xffffffffu, rowbits, 4 * q + i) << (8 * i);
+        w[q] = x;
       }
-      const unsigned b0 = __ballot_sync(0xffffffffu, mc[0]);
-      const unsigned b1 = __ballot_sync(0xffffffffu, mc[1]);
+      const bool active = (w[0] | w[1] | w[2] | w[3]) != 0;
       if (lane == 0) {
-        info[slot].bits[warp - 10] = b0;       // pixels 0-31 / 32-63
-        info[slot].bits[warp - 8] = b1;        // pixels 64-95 / 96-127
-      }
-      tc::named_bar_sync(3, 64);
-      const uint32_t* bits = info[slot].bits;
-      const bool active = (bits[0] | bits[1] | bits[2] | bits[3]) != 0;
-      if (lt == 0) {
         ++n_tot;
         if (active) {
           ++n_dense;
-          n_mc += __popc(bits[0]) + __popc(bits[1]) + __popc(bits[2]) + __popc(bits[3]);
+          n_mc += __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
         } else {
           ++n_skip;
         }
@@ -260,25 +294,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       if (!active) {
         // "independent of whether a tile is skipped, we write the update mask"
         if (rank == 0)
-          for (int m = lt; m < 128; m += 64) {
+          for (int m = lane; m < 128; m += 32) {
             const int oy = ty * 16 + (m >> 3), ox = tx * 8 + (m & 7);
             if (oy < p.Ho && ox < p.Wo) p.ep.mask[((long long)s * p.Ho + oy) * p.Wo + ox] = 0;
           }
         continue;                              // slot stays owned for the next tile
       }
-      if (lt == 0) {
+      if (lane == 0) {
+        info[slot].bits[0] = w[0];
+        info[slot].bits[1] = w[1];
+        info[slot].bits[2] = w[2];
+        info[slot].bits[3] = w[3];
         info[slot].tile = tile;
-        tc::mbar_arrive(&info_full[slot]);
+        tc::mbar_arrive(&info_full[slot]);     // release: hm and bits visible to the consumers
       }
-      TCTR(lt == 0 && v == 0, 4);
+      TCTR(lane == 0 && v == 0, 4);
       ++v;
       own = false;
     }
     // terminator
     const int slot = v % TC_NI;
     if (!own) tc::mbar_wait(&info_empty[slot], ((v / TC_NI) & 1) ^ 1);
-    tc::named_bar_sync(3, 64);
-    if (lt == 0) {
+    __syncwarp();
+    if (lane == 0) {
       info[slot].tile = -1;
       tc::mbar_arrive(&info_full[slot]);
       if (p.fused && rank == 0 && p.tstats) {
@@ -288,19 +326,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         atomicAdd(&p.tstats[6], n_mc);
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp == 8) {
     // ---------------------------------------------------------------- halo loaders
     // One elected lane issues the TMA tensor copies of a (tile, channel block) group (one
     // per stride phase; out-of-image pixels are zero-filled by the copy).  Once a group has
     // landed, every loader thread zeroes the pixels whose update-mask bit is 0 -- step (a)
     // of PAPER.md:654 "store zero values for inputs which were not updated" -- so stale
     // deltas never reach an MMA.  Group k-1 is finished while group k is in flight.
-    const int lt = tid - 128;
+    const int lt = lane;
     const int nch = p.BK / 8;
     const int npx = p.HH * p.WW;
     const int lgs = p.stride == 2 ? 1 : 0;
     const uint32_t gbytes = (uint32_t)(p.stride * nch * p.HH * p.WQ * 16);   // bytes the boxes write
-    const int hy_0 = lt / p.WW, hx_0 = lt - hy_0 * p.WW, dy128 = 128 / p.WW, dx128 = 128 - dy128 * p.WW;
+    const int hy_0 = lt / p.WW, hx_0 = lt - hy_0 * p.WW, dy32 = 32 / p.WW, dx32 = 32 - dy32 * p.WW;
     int k = 0;                                 // global group counter
     int pg_slot = 0, pg_iy0 = 0, pg_ix0 = 0;   // tile of group k-1
     bool pg_last = false;
@@ -310,15 +348,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       const uint8_t* hm = smem + L.hmask + pg_slot * TC_HMASK_BYTES;
       unsigned char* A = smem + L.a0 + b * p.a_bytes;
       int hy = hy_0, hx = hx_0;
-      for (int px = lt; px < npx; px += 128) {
+      for (int px = lt; px < npx; px += 32) {
         const int iy = pg_iy0 + hy, ix = pg_ix0 + hx;
         if (!hm[px] && iy >= 0 && iy < p.H && ix >= 0 && ix < p.W) {
           unsigned char* d = A + (hx & lgs) * p.phase_bytes + (hy * p.WQ + (hx >> lgs)) * 16;
           for (int ch = 0; ch < nch; ++ch)
             *reinterpret_cast<uint4*>(d + ch * p.plane) = make_uint4(0u, 0u, 0u, 0u);
         }
-        hx += dx128;
-        hy += dy128;
+        hx += dx32;
+        hy += dy32;
         if (hx >= p.WW) { hx -= p.WW; ++hy; }
       }
       tc::fence_proxy_async_smem();            // generic-proxy zeros -> tensor-core reads
@@ -355,7 +393,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     }
     if (k > 0) finish(k - 1);
     TCTR(lt == 0, 6);
-  } else if (warp == 8) {
+  } else if (warp == 9) {
     // ---------------------------------------------------------------- weight producer
     // resident: everything was issued above; streaming: the first npre steps were issued
     // speculatively for the first active tile, the rest follow the ring
@@ -387,7 +425,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       const int st = p.resident ? jj % nsteps : jj % p.stages;
       tc::mbar_wait(&b_full[st], p.resident ? 0 : (jj / p.stages) & 1);
     }
-  } else if (warp == 9) {
+  } else if (warp == 10) {
     // ---------------------------------------------------------------- MMA issuer
     // warp-uniform loop; descriptors live in uniform registers, one elected lane issues
     const uint32_t sbo_a = (uint32_t)(p.stride * p.WQ * 16);   // next output row = stride halo rows
@@ -435,6 +473,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             if (!p.resident) tc::mma_commit(&b_empty[st]);   // stage reusable once these finish
           }
           __syncwarp();
+          TCTR(lane == 0 && j == 0, 24);
         }
         if (tc::elect_one()) tc::mma_commit(&a_empty[b]);   // halo buffer reusable
         __syncwarp();
@@ -445,55 +484,90 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       ++u;
     }
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 0-3)
-    // thread = TMEM lane = output pixel; Eqs. 4-6 with the per-pixel max-norm computed
-    // in registers (pass 1), then caches / delta / output written (pass 2).  The cache
-    // rows of the first 64 channels are loaded while the MMAs still run.
+    // ---------------------------------------------------------------- epilogue (warps 0-7)
+    // thread = (TMEM lane = output pixel, half of the CTA's output channels).  Pass 1 forms
+    // s = x^A + x^T + dx and d = f(s) - f(x^A) (Eqs. 5-6) and the pixel's max-norm; the two
+    // halves combine through smem, cluster partners through DSMEM (Eq. 4 decision).  Pass 2
+    // writes caches, delta and output.  The first 32 channels of each half keep d in
+    // registers between the passes, and their cache rows are loaded while the MMAs run.
     const Epi& e = p.ep;
-    const int Cg = e.C;                       // channels of the output rows (pitch)
-    const int cb0 = rank * p.Ns;              // this CTA's first output channel
-    const int C = min(p.Ns, Cg - cb0);        // this CTA's channels
+    const int q4 = warp & 3, half = warp >> 2;
+    const int m = q4 * 32 + lane;              // output pixel of the tile = TMEM lane
+    const int Cg = e.C;                        // channels of the output rows (pitch)
+    const int cb0 = rank * p.Ns;               // this CTA's first output channel
+    const int Ccta = min(p.Ns, Cg - cb0);      // this CTA's channels
+    const int CH = ((Ccta + 31) / 32) * 16;    // channels of half 0 (multiple of 16)
+    const int c_lo = half ? CH : 0;            // my first channel (relative to cb0)
+    const int C = half ? max(0, Ccta - CH) : min(CH, Ccta);   // my channel count
     const bool vec = (Cg % 8) == 0;
     const float eps = *e.eps;
-    const float* bias = p.bias + cb0;
+    const float* bias = p.bias + cb0 + c_lo;
+    float* pm2 = reinterpret_cast<float*>(smem + L.pm2);   // [2][2][128] half partial norms
     constexpr bool trunc = ACT != ACT_NONE;
-    constexpr bool half_cache = sizeof(TC) == 2;
-    constexpr int PF = half_cache ? 8 : 0;    // prefetched 8-channel chunks (64 channels)
+    constexpr int PF = sizeof(TC) == 2 ? 4 : 0;   // prefetched 8-channel chunks (32 channels)
     unsigned nact = 0;
     int u = 0;
     for (int v = 0;; ++v) {
       const int slot = v % TC_NI;
       tc::mbar_wait(&info_full[slot], (v / TC_NI) & 1);
       const int tile = info[slot].tile;
-      const bool mcb = tile >= 0 && ((info[slot].bits[tid >> 5] >> (tid & 31)) & 1u);   // m_conv of my pixel
+      const bool mcb = tile >= 0 && ((info[slot].bits[q4] >> lane) & 1u);   // m_conv of my pixel
       tc::mbar_arrive(&info_empty[slot]);
       if (tile < 0) break;
       const int s = tile / (p.nty * p.ntx);
       const int ty = (tile / p.ntx) % p.nty, tx = tile % p.ntx;
-      const int oy = ty * 16 + tid / 8, ox = tx * 8 + tid % 8;
+      const int oy = ty * 16 + (m >> 3), ox = tx * 8 + (m & 7);
       const bool inb = oy < p.Ho && ox < p.Wo;
       const long long pix = ((long long)s * p.Ho + oy) * p.Wo + ox;
       const bool act = inb && mcb;
       const bool first = e.first[s] != 0;
-      __half* dl = reinterpret_cast<__half*>(e.delta) + pix * Cg + cb0;
-      float* O = e.O ? e.O + pix * Cg + cb0 : nullptr;
-      TC* A = reinterpret_cast<TC*>(e.xA) + pix * Cg + cb0;
-      TC* Tt = reinterpret_cast<TC*>(e.xT) + pix * Cg + cb0;
+      const long long row = pix * Cg + cb0 + c_lo;
+      __half* dl = reinterpret_cast<__half*>(e.delta) + row;
+      float* O = e.O ? e.O + row : nullptr;
+      TC* A = reinterpret_cast<TC*>(e.xA) + row;
+      TC* Tt = reinterpret_cast<TC*>(e.xT) + row;
       const bool full_rows = vec && (C % 8) == 0;
-      // ---- loads that do not depend on the accumulator
-      uint4 ra[PF > 0 ? PF : 1], rt[PF > 0 ? PF : 1];
-      if (act && trunc && !first) {
-        if constexpr (PF > 0) {
-          if (full_rows) {
-#pragma unroll
-            for (int q = 0; q < PF; ++q)
-              if (8 * q < C) {
-                ra[q] = *reinterpret_cast<const uint4*>(A + 8 * q);
-                rt[q] = *reinterpret_cast<const uint4*>(Tt + 8 * q);
-              }
+      // ---- coalesced row access (fp16 rows) through this warp's staging areas SA / ST / SD
+      // (32 pixels x 80 B each): lane l of a global load/store instruction i moves 16-B
+      // chunk (l mod lp) of pixel (i*32/lp + l/lp), so one instruction covers 32/lp pixel
+      // rows of lp*16 contiguous bytes (lane-per-pixel access would touch 32 lines).  Each
+      // lane then works on its own pixel's row in smem.  Loops are deliberately not
+      // unrolled: at S = 1 every tile runs cold code, so code size is latency.
+      constexpr bool COAL = sizeof(TC) == 2;
+      const bool coal = COAL && full_rows;
+      unsigned char* SA = smem + L.stage + warp * TC_STAGE_WARP;
+      unsigned char* ST = SA + 32 * 80;
+      unsigned char* SD = ST + 32 * 80;
+      const long long pixw = ((long long)s * p.Ho + ty * 16 + q4 * 4) * p.Wo + tx * 8;   // pixel 0 of the warp
+      // move the n16 16-B chunks of the rows of the pixels in pm between global rows
+      // (base + pix * Cg) and a staging area; dir 0 = load into smem, 1 = store from smem
+      // (dir 1: pixels in zm store zeros instead of the staged row)
+      auto stage_move = [&](unsigned char* area, __half* base, int n16, uint32_t pm, int dir, uint32_t zm = 0u) {
+        const int lg = n16 > 2 ? 2 : n16 - 1, lp = 1 << lg;
+        __syncwarp();
+#pragma unroll 1
+        for (int i = 0; i < lp; ++i) {
+          const int pl = (i << (5 - lg)) + (lane >> lg), c = lane & (lp - 1);
+          if (c < n16 && ((pm >> pl) & 1u)) {
+            uint4* g = reinterpret_cast<uint4*>(base + (pixw + (long long)(pl >> 3) * p.Wo + (pl & 7)) * Cg + c * 8);
+            uint4* sm = reinterpret_cast<uint4*>(area + pl * 80 + c * 16);
+            if (dir) *g = ((zm >> pl) & 1u) ? make_uint4(0u, 0u, 0u, 0u) : *sm;
+            else *sm = *g;
           }
         }
-        for (int c = 8 * PF; c < C; c += 64 / (int)sizeof(TC)) { prefetch_l2(A + c); prefetch_l2(Tt + c); }
+        __syncwarp();
+      };
+      const uint32_t actm = __ballot_sync(0xffffffffu, act);
+      const long long chan0 = cb0 + c_lo;       // my first channel in the row
+      __half* gA = reinterpret_cast<__half*>(e.xA) + chan0;
+      __half* gT = reinterpret_cast<__half*>(e.xT) + chan0;
+      __half* gD = reinterpret_cast<__half*>(e.delta) + chan0;
+      auto n16_of = [&](int sl) { return C - sl >= 32 ? 4 : (C - sl) / 8; };
+      const bool need_cache = trunc && !first;
+      // ---- loads that do not depend on the accumulator: the first slice of the cache rows
+      if (need_cache && coal && actm && C > 0) {
+        stage_move(SA, gA, n16_of(0), actm, 0);
+        stage_move(ST, gT, n16_of(0), actm, 0);
       }
       if (act && O && !first)
         for (int c = 0; c < C; c += 32) prefetch_l2(O + c);
@@ -502,160 +576,186 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       tc::mbar_wait(&acc_full[acc], (u >> 1) & 1);
       tc::tc_fence_after();
       TCTR(tid == 0 && u == 0, 11);
-      const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * p.acc_stride);
-      bool upd = act;
-      // a, t of 16 channels [c0, c0+16): from the prefetched registers when possible
-      auto cache16 = [&](int c0, float a[16], float t[16]) {
-        if (!(trunc && !first)) {
+      const uint32_t tbase = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * p.acc_stride + c_lo);
+      // one 8-channel chunk [c0, c0+8): z from TMEM (+ bias on a first frame), a and t from
+      // the staging areas (coal) or the cache rows
+      auto chunk_in = [&](int c0, float z[8], float a[8], float t[8]) {
+        uint32_t r[8];
+        tc::tmem_ld8(tbase + c0, r);            // warp-collective
+        tc::tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < 16; ++k) a[k] = t[k] = 0.f;
-          return;
+        for (int k = 0; k < 8; ++k) {
+          z[k] = __uint_as_float(r[k]);
+          if (first) z[k] += c0 + k < C ? bias[c0 + k] : 0.f;
+          a[k] = t[k] = 0.f;
         }
-        if constexpr (PF > 0) {
-          if (full_rows && c0 < 8 * PF) {
-            // constant register indices only, so ra/rt never go to local memory
-            const int h = c0 >> 4;
-            const uint4 a0 = h == 0 ? ra[0] : h == 1 ? ra[2] : h == 2 ? ra[4] : ra[6];
-            const uint4 a1 = h == 0 ? ra[1] : h == 1 ? ra[3] : h == 2 ? ra[5] : ra[7];
-            const uint4 t0 = h == 0 ? rt[0] : h == 1 ? rt[2] : h == 2 ? rt[4] : rt[6];
-            const uint4 t1 = h == 0 ? rt[1] : h == 1 ? rt[3] : h == 2 ? rt[5] : rt[7];
-            unpack8<TC>(a0, a);
-            unpack8<TC>(t0, t);
-            if (c0 + 8 < C) {
-              unpack8<TC>(a1, a + 8);
-              unpack8<TC>(t1, t + 8);
-            } else {
-#pragma unroll
-              for (int k = 8; k < 16; ++k) a[k] = t[k] = 0.f;
-            }
-            return;
-          }
-        }
-        if (full_rows) {
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            if (c0 + 8 * q < C) {
-              ld8(A + c0 + 8 * q, a + 8 * q);
-              ld8(Tt + c0 + 8 * q, t + 8 * q);
-            } else {
-#pragma unroll
-              for (int k = 0; k < 8; ++k) a[8 * q + k] = t[8 * q + k] = 0.f;
-            }
-          }
+        if (!act || !need_cache) return;
+        if (coal) {
+          const int off = lane * 80 + (c0 & 31) * 2;
+          unpack8<__half>(*reinterpret_cast<const uint4*>(SA + off), a);
+          unpack8<__half>(*reinterpret_cast<const uint4*>(ST + off), t);
         } else {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
+          for (int k = 0; k < 8; ++k) {
             a[k] = c0 + k < C ? ld(A + c0 + k) : 0.f;
             t[k] = c0 + k < C ? ld(Tt + c0 + k) : 0.f;
           }
         }
       };
-      auto zload = [&](int c0, float z[16]) {      // warp-collective: every lane loads
-        uint32_t r0[16];
-        tc::tmem_ld16(tbase + c0, r0);
-        tc::tmem_wait_ld();
-#pragma unroll
-        for (int k = 0; k < 16; ++k) z[k] = __uint_as_float(r0[k]);
-        if (first) {
-#pragma unroll
-          for (int k = 0; k < 16; ++k) z[k] += c0 + k < C ? bias[c0 + k] : 0.f;
-        }
-      };
+      bool upd = act;
+      // <= 32 channels per thread with coalesced rows: one pass (pass 1 stages both outcomes)
+      const bool single = trunc && coal && C > 0 && C <= 32;
       if (trunc) {
         float mx = 0.f;
-        for (int c0 = 0; c0 < C; c0 += 16) {
-          float z[16];
-          zload(c0, z);
+#pragma unroll 1
+        for (int c0 = 0; c0 < C; c0 += 8) {
+          if (coal && need_cache && actm && c0 > 0 && (c0 & 31) == 0) {   // next slice
+            stage_move(SA, gA + c0, n16_of(c0), actm, 0);
+            stage_move(ST, gT + c0, n16_of(c0), actm, 0);
+          }
+          float z[8], a[8], t[8];
+          chunk_in(c0, z, a, t);
           if (act) {
-            float a[16], t[16];
-            cache16(c0, a, t);
+            float o[8];
 #pragma unroll
-            for (int k = 0; k < 16; ++k)
-              if (c0 + k < C) {
-                const float prev = first ? 0.f : act_t<ACT>(a[k], e.act_param);
-                mx = fmaxf(mx, fabsf(act_t<ACT>(a[k] + t[k] + z[k], e.act_param) - prev));
-              }
+            for (int k = 0; k < 8; ++k) {
+              const float prev = first ? 0.f : act_t<ACT>(a[k], e.act_param);
+              const float sv = a[k] + t[k] + z[k];
+              const float d = act_t<ACT>(sv, e.act_param) - prev;
+              if (c0 + k < C) mx = fmaxf(mx, fabsf(d));
+              o[k] = d;
+              a[k] = sv;                       // x^A if updated (Eq. 6)
+              t[k] += z[k];                    // x^T if truncated
+            }
+            if (single) {                      // both outcomes staged in place; the flush picks
+              const int off = lane * 80 + c0 * 2;
+              *reinterpret_cast<uint4*>(SD + off) =
+                  make_uint4(pack_h2(o[0], o[1]), pack_h2(o[2], o[3]), pack_h2(o[4], o[5]), pack_h2(o[6], o[7]));
+              *reinterpret_cast<uint4*>(SA + off) =
+                  make_uint4(pack_h2(a[0], a[1]), pack_h2(a[2], a[3]), pack_h2(a[4], a[5]), pack_h2(a[6], a[7]));
+              *reinterpret_cast<uint4*>(ST + off) =
+                  make_uint4(pack_h2(t[0], t[1]), pack_h2(t[2], t[3]), pack_h2(t[4], t[5]), pack_h2(t[6], t[7]));
+            }
           }
         }
+        TCTR(tid == 0 && u == 0, 15);
+        // max-norm over the pixel's channels: the two halves of this CTA ...
+        const int xb = u & 1;
+        pm2[xb * 256 + half * 128 + m] = mx;
+        tc::named_bar_sync(2, 256);
+        mx = fmaxf(pm2[xb * 256 + m], pm2[xb * 256 + 128 + m]);
         if (nsplit > 1) {
-          // per-pixel max-norm over all output channels of the cluster (DSMEM exchange)
-          const int xb = u & 1;
-          pmax[xb * 128 + tid] = mx;
-          tc::named_bar_sync(2, 128);
+          // ... and every CTA of the cluster (DSMEM exchange)
+          if (half == 0) pmax[xb * 128 + m] = mx;
+          tc::named_bar_sync(2, 256);
           if (tid == 0) {
             const uint32_t local = tc::smem_u32(&xch[xb]);
             for (int r = 0; r < nsplit; ++r) tc::mbar_arrive_remote(tc::mapa(local, (uint32_t)r));
           }
           tc::mbar_wait_cluster(&xch[xb], (u >> 1) & 1);
-          const uint32_t mine = tc::smem_u32(&pmax[xb * 128 + tid]);
+          const uint32_t mine = tc::smem_u32(&pmax[xb * 128 + m]);
           for (int r = 0; r < nsplit; ++r) mx = fmaxf(mx, tc::ld_dsmem_f32(tc::mapa(mine, (uint32_t)r)));
         }
         upd = act && (first || eps < 0.f || mx > eps);
       }
-      for (int c0 = 0; c0 < C; c0 += 16) {
-        float z[16];
-        zload(c0, z);
-        if (!act) continue;
-        float a[16], t[16];
-        if (trunc) cache16(c0, a, t);
-        const bool full = vec && c0 + 16 <= C;
-        if (trunc && !upd) {                                                  // x^T += dx
-#pragma unroll
-          for (int k = 0; k < 16; ++k) t[k] += z[k];
-          if (full) {
-            st8(Tt + c0, t);
-            st8(Tt + c0 + 8, t + 8);
-          } else {
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-              if (c0 + k < C) st(Tt + c0 + k, t[k]);
-          }
-          continue;
+      TCTR(tid == 0 && u == 0, 16);
+      const uint32_t updm = __ballot_sync(0xffffffffu, upd);
+      // ---- pass 2: results of each 32-channel slice staged in SA (x^A), ST (x^T), SD (delta),
+      // then flushed with coalesced stores
+#pragma unroll 1
+      for (int c0 = single ? (C - 1) & ~7 : 0; c0 < C; c0 += 8) {
+        if (single) goto flush;                  // results already staged by pass 1
+        if (coal && need_cache && actm && (c0 & 31) == 0 && (c0 > 0 || C > 32)) {   // reload the slice
+          stage_move(SA, gA + c0, n16_of(c0), actm, 0);
+          stage_move(ST, gT + c0, n16_of(c0), actm, 0);
         }
-        float o[16];
+        float z[8], a[8], t[8], o[8];
+        chunk_in(c0, z, a, t);
+        if (act) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          if (trunc) {
-            const float sv = a[k] + t[k] + z[k];                                // Eq. 6
-            const float prev = first ? 0.f : act_t<ACT>(a[k], e.act_param);
-            o[k] = __half2float(__float2half_rn(act_t<ACT>(sv, e.act_param) - prev));
-            a[k] = sv;
-          } else {
-            o[k] = __half2float(__float2half_rn(z[k]));
-          }
-        }
-        if (full) {
-#pragma unroll
-          for (int k = 0; k < 16; k += 8) {
-            st8(dl + c0 + k, o + k);
-            if (trunc) { st8(A + c0 + k, a + k); st8_zero(Tt + c0 + k); }
-          }
-          if (O) {
-            if (first) {
-              st8(O + c0, o);
-              st8(O + c0 + 8, o + 8);
+          for (int k = 0; k < 8; ++k) {
+            if (trunc) {
+              const float prev = first ? 0.f : act_t<ACT>(a[k], e.act_param);
+              const float sv = a[k] + t[k] + z[k];
+              o[k] = rnd<__half>(act_t<ACT>(sv, e.act_param) - prev);
+              if (upd) { a[k] = sv; t[k] = 0.f; }                 // Eq. 6: x^A := s
+              else t[k] += z[k];                                   // x^T += dx
             } else {
-              float ov[16];
-              ld8(O + c0, ov);
-              ld8(O + c0 + 8, ov + 8);
-#pragma unroll
-              for (int k = 0; k < 16; ++k) ov[k] += o[k];
-              st8(O + c0, ov);
-              st8(O + c0 + 8, ov + 8);
+              o[k] = rnd<__half>(z[k]);
             }
           }
-        } else {
+          if (O && upd && !coal) {
+            float ov[8];
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            if (c0 + k >= C) continue;
-            st(dl + c0 + k, o[k]);
-            if (trunc) { st(A + c0 + k, a[k]); st(Tt + c0 + k, 0.f); }
-            if (O) O[c0 + k] = first ? o[k] : O[c0 + k] + o[k];
+            for (int k = 0; k < 8; ++k) ov[k] = (c0 + k < C && !first) ? O[c0 + k] : 0.f;   // loads first
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (c0 + k < C) O[c0 + k] = ov[k] + o[k];
+          }
+          if (coal) {
+            const int off = lane * 80 + (c0 & 31) * 2;
+            *reinterpret_cast<uint4*>(SD + off) =
+                make_uint4(pack_h2(o[0], o[1]), pack_h2(o[2], o[3]), pack_h2(o[4], o[5]), pack_h2(o[6], o[7]));
+            if (trunc) {
+              *reinterpret_cast<uint4*>(SA + off) =
+                  make_uint4(pack_h2(a[0], a[1]), pack_h2(a[2], a[3]), pack_h2(a[4], a[5]), pack_h2(a[6], a[7]));
+              *reinterpret_cast<uint4*>(ST + off) =
+                  make_uint4(pack_h2(t[0], t[1]), pack_h2(t[2], t[3]), pack_h2(t[4], t[5]), pack_h2(t[6], t[7]));
+            }
+          } else {
+            // direct per-pixel stores (fp32 caches or channel counts that are not multiples of 8)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              if (c0 + k >= C) continue;
+              if (trunc) {
+                st(Tt + c0 + k, t[k]);
+                if (upd) st(A + c0 + k, a[k]);
+              }
+              if (upd) st(dl + c0 + k, o[k]);
+            }
+          }
+        }
+      flush:
+        if (coal && ((c0 & 31) == 24 || c0 + 8 >= C)) {   // slice complete: flush
+          const int sl = c0 & ~31, n16 = n16_of(sl);
+          TCTR(tid == 0 && u == 0 && sl == 0, 19);
+          if (trunc) {
+            stage_move(SA, gA + sl, n16, updm, 1);
+            TCTR(tid == 0 && u == 0 && sl == 0, 20);
+            stage_move(ST, gT + sl, n16, actm, 1, updm);   // x^T := 0 where updated
+          }
+          TCTR(tid == 0 && u == 0 && sl == 0, 21);
+          stage_move(SD, gD + sl, n16, updm, 1);
+          TCTR(tid == 0 && u == 0 && sl == 0, 22);
+          if (O && updm) {
+            // a8 (output accumulation) O += delta for the slice, coalesced: 8 lanes per pixel
+            // row of 32 fp32 channels, all loads of the slice in flight before the stores
+            float* Ob = e.O + chan0 + sl;
+            float4 ov[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int pl = (i << 2) + (lane >> 3), c4 = lane & 7;
+              ov[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (4 * c4 < 8 * n16 && ((updm >> pl) & 1u) && !first)
+                ov[i] = *reinterpret_cast<const float4*>(Ob + (pixw + (long long)(pl >> 3) * p.Wo + (pl & 7)) * Cg + 4 * c4);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int pl = (i << 2) + (lane >> 3), c4 = lane & 7;
+              if (4 * c4 < 8 * n16 && ((updm >> pl) & 1u)) {
+                const uint2 h = *reinterpret_cast<const uint2*>(SD + pl * 80 + c4 * 8);
+                const float2 d01 = unpack_h2(h.x), d23 = unpack_h2(h.y);
+                ov[i].x += d01.x; ov[i].y += d01.y; ov[i].z += d23.x; ov[i].w += d23.y;
+                *reinterpret_cast<float4*>(Ob + (pixw + (long long)(pl >> 3) * p.Wo + (pl & 7)) * Cg + 4 * c4) = ov[i];
+              }
+            }
+            __syncwarp();
           }
         }
       }
-      if (inb && rank == 0) e.mask[pix] = upd ? 1 : 0;     // final mask of every tile pixel
-      nact += (upd && rank == 0) ? 1 : 0;
+      TCTR(tid == 0 && u == 0, 17);
+      if (inb && rank == 0 && half == 0) e.mask[pix] = upd ? 1 : 0;   // final mask of every tile pixel
+      nact += (upd && rank == 0 && half == 0) ? 1 : 0;
       TCTR(tid == 0 && u == 0, 12);
       tc::tc_fence_before();
       tc::mbar_arrive(&acc_empty[acc]);
@@ -669,7 +769,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   if (nsplit > 1) tc::cluster_sync_all();     // partners may still read our smem
   else __syncthreads();
   TCTR(threadIdx.x == 0, 14);
-  if (warp == 9) {
+  if (warp == 10) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, p.tmem_cols);
   }
