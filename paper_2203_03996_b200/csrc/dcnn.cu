@@ -306,7 +306,8 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
   ip.eps = n->eps; ip.first = n->first; ip.err = n->err; ip.n_active = n->stats + 1;
   {
     TimeScope ts(n, st, DCNN_KCLASS_INPUT);
-    launch_input(ip, n->dtype, st);
+    if (ip.radius == 0 && ip.C <= 4) launch_input_r0(ip, n->dtype, st);
+    else launch_input(ip, n->dtype, st);
   }
   ++k;
   if (!n->aux.empty()) cudaEventRecord(n->ev_input, st);
@@ -413,12 +414,15 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       pp.vec = vec ? 1 : 0;
       pp.G = group_lanes(o.C);
       pp.ep = make_epi(n, i);
+      const bool lean_pool = lean_pool_ok(pp, n->dtype);
       {
         TimeScope ts(n, ost, DCNN_KCLASS_POINTWISE);
-        launch_pointwise(pp, n->dtype, n->cache32, ost);
+        if (lean_pool) launch_maxpool_disj(pp, n->cache32, ost);       // pool + A update, one launch
+        else if (lean_up_ok(pp, n->dtype)) launch_up_lean(pp, ost);
+        else launch_pointwise(pp, n->dtype, n->cache32, ost);
       }
       ++k;
-      if (o.kind == DCNN_OP_MAXPOOL) {
+      if (o.kind == DCNN_OP_MAXPOOL && !lean_pool) {
         TimeScope ts(n, ost, DCNN_KCLASS_POINTWISE);
         launch_pool_update(pp, n->dtype, n->cache32, ost);
         ++k;

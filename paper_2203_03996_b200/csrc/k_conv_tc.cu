@@ -342,9 +342,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     int k = 0;                                 // global group counter
     int pg_slot = 0, pg_iy0 = 0, pg_ix0 = 0;   // tile of group k-1
     bool pg_last = false;
+    int b0_extra = 0;                          // extra completed phases of a_tma[0] (drained speculation)
     auto finish = [&](int kk) {                // zero inactive pixels of group kk, publish it
       const int b = kk % NA;
-      tc::mbar_wait(&a_tma[b], (kk / NA) & 1);
+      tc::mbar_wait(&a_tma[b], ((kk / NA) + (b == 0 ? b0_extra : 0)) & 1);
       const uint8_t* hm = smem + L.hmask + pg_slot * TC_HMASK_BYTES;
       unsigned char* A = smem + L.a0 + b * p.a_bytes;
       int hy = hy_0, hx = hx_0;
@@ -363,26 +364,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       tc::mbar_arrive(&a_full[b]);
       if (pg_last) tc::mbar_arrive(&info_empty[pg_slot]);   // hmask of that slot no longer read
     };
+    // issue the TMA copies of channel block cb of a tile into buffer b
+    auto issue = [&](int b, int tile, int cb) {
+      if (lt == 0) {
+        const int s = tile / (p.nty * p.ntx);
+        const int ty = (tile / p.ntx) % p.nty, tx = tile % p.ntx;
+        const int iy0 = ty * 16 * p.stride - p.pad, ix0 = tx * 8 * p.stride - p.pad;
+        tc::mbar_arrive_expect_tx(&a_tma[b], gbytes);
+        const uint32_t A = tc::smem_u32(smem + L.a0 + b * p.a_bytes);
+        // one box of 8 channels x (columns of one stride phase) x halo rows per plane
+        for (int ph = 0; ph < p.stride; ++ph)
+          for (int ch = 0; ch < nch; ++ch)
+            tma_load_4d(A + ph * p.phase_bytes + ch * p.plane, &p.tmap, cb * p.BK + ch * 8, ix0 + ph, iy0, s,
+                        &a_tma[b]);
+      }
+    };
+    // speculation: the first tile of this CTA is usually its first active one (at S = 1 a
+    // layer rarely has more tiles than CTAs), so its first halo block is fetched right away,
+    // in parallel with the scout's mask check; a wrong guess only costs the drained copy
+    const int spec_tile = cid < count ? tile_of(cid) : -1;
+    bool spec = spec_tile >= 0;
+    if (spec) issue(0, spec_tile, 0);
     for (int v = 0;; ++v) {
       const int slot = v % TC_NI;
       tc::mbar_wait(&info_full[slot], (v / TC_NI) & 1);
       const int tile = info[slot].tile;
+      if (spec && tile != spec_tile) {         // wrong guess: let the copy land, then reuse buffer 0
+        tc::mbar_wait(&a_tma[0], 0);
+        b0_extra = 1;
+        spec = false;
+      }
       if (tile < 0) break;
       const int s = tile / (p.nty * p.ntx);
       const int ty = (tile / p.ntx) % p.nty, tx = tile % p.ntx;
       const int iy0 = ty * 16 * p.stride - p.pad, ix0 = tx * 8 * p.stride - p.pad;
+      (void)s;
       for (int cb = 0; cb < p.ncb; ++cb, ++k) {
         const int b = k % NA;
         tc::mbar_wait(&a_empty[b], ((k / NA) & 1) ^ 1);
-        if (lt == 0) {
-          tc::mbar_arrive_expect_tx(&a_tma[b], gbytes);
-          const uint32_t A = tc::smem_u32(smem + L.a0 + b * p.a_bytes);
-          // one box of 8 channels x (columns of one stride phase) x halo rows per plane
-          for (int ph = 0; ph < p.stride; ++ph)
-            for (int ch = 0; ch < nch; ++ch)
-              tma_load_4d(A + ph * p.phase_bytes + ch * p.plane, &p.tmap, cb * p.BK + ch * 8, ix0 + ph, iy0, s,
-                          &a_tma[b]);
-        }
+        if (spec && k == 0) spec = false;      // already in flight
+        else issue(b, tile, cb);
         TCTR(lt == 0 && k == 0, 5);
         if (k > 0) finish(k - 1);
         pg_slot = slot;
@@ -431,6 +452,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const uint32_t sbo_a = (uint32_t)(p.stride * p.WQ * 16);   // next output row = stride halo rows
     const uint32_t lbo_b = (uint32_t)(p.Ns * 16);
     const uint32_t idesc = tc::idesc_f16(128, p.Ns);
+    const uint64_t a_step = (uint64_t)((2 * p.plane) >> 4), b_step = (uint64_t)(2 * p.Ns);
+    const int nk = p.BK / 16;
     int j = 0, k = 0, u = 0;
     for (int v = 0;; ++v) {
       const int slot = v % TC_NI;
@@ -459,15 +482,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           const uint32_t bbase = tc::smem_u32(bstage + (size_t)st * p.b_bytes);
           if (tc::elect_one()) {
             // all MMAs of tg taps x BK/16 K-steps against one weight step
+            uint32_t accum = (cb | g) != 0;
             for (int t = 0; t < p.tg; ++t) {
-              const int tap = g * p.tg + t;
-              const uint64_t ad0 = tc::smem_desc(abase + tapoff[tap], p.plane, sbo_a);
-              const uint64_t bd0 = tc::smem_desc(bbase + (uint32_t)(t * p.Ns * p.BK * 2), lbo_b, 128);
-              for (int kc = 0; kc < p.BK / 16; ++kc) {
-                // start-address fields advance by 2 planes (A) / 2 chunks (B) per K = 16
-                const uint64_t ad = ad0 + (uint64_t)((2 * kc * p.plane) >> 4);
-                const uint64_t bd = bd0 + (uint64_t)((2 * kc * p.Ns * 16) >> 4);
-                tc::mma_f16(dbase, ad, bd, idesc, (cb | tap | kc) != 0);
+              uint64_t ad = tc::smem_desc(abase + tapoff[g * p.tg + t], p.plane, sbo_a);
+              uint64_t bd = tc::smem_desc(bbase + (uint32_t)(t * p.Ns * p.BK * 2), lbo_b, 128);
+              for (int kc = 0; kc < nk; ++kc) {
+                tc::mma_f16(dbase, ad, bd, idesc, accum);
+                accum = 1;
+                ad += a_step;                    // start address: + 2 planes (A) per K = 16
+                bd += b_step;                    // + 2 core-matrix chunks (B)
               }
             }
             if (!p.resident) tc::mma_commit(&b_empty[st]);   // stage reusable once these finish
@@ -504,7 +527,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const float* bias = p.bias + cb0 + c_lo;
     float* pm2 = reinterpret_cast<float*>(smem + L.pm2);   // [2][2][128] half partial norms
     constexpr bool trunc = ACT != ACT_NONE;
-    constexpr int PF = sizeof(TC) == 2 ? 4 : 0;   // prefetched 8-channel chunks (32 channels)
     unsigned nact = 0;
     int u = 0;
     for (int v = 0;; ++v) {

@@ -1,0 +1,226 @@
+// k_lean.cu -- latency-lean variants of a1 (input delta), a7 (max-pool) and a6 (nearest
+// upsample) for the common shapes.  At one stream per GPU a frame is a chain of small
+// dependent kernels, so each kernel is built to finish in ONE global round trip: every
+// load a thread may need (update masks, deltas, cached accumulations) is issued at once,
+// before any of them is inspected.  Loading a delta whose mask bit turns out to be 0 is
+// harmless -- the value is discarded by a select, never used in arithmetic (stale data,
+// PAPER.md:255).
+//
+//   k_input_r0        a1 with no input dilation (r = 0): one thread per pixel
+//   k_maxpool_disj    a7 for disjoint windows (k == stride, pad 0, map divisible by k):
+//                     Eq. 3 AND the accumulated-input update A += dx in
+//                     the same thread (every input pixel belongs to exactly one window)
+//   k_up_lean         a6 nearest upsample: out(p) = in(p / f) for delta and mask (Z11)
+#include "kernels.h"
+
+namespace dcnn {
+
+// ---------------------------------------------------------------- a1, r = 0
+// PAPER.md:129 "Delta Generation subtracts the previous input from the current";
+// m = [max_c |F - P| > eps_in] (strict, Z1); on m: delta = F - P, P := F.  First frame:
+// delta = F, m = 1, P = F.  C <= 4 (camera frames).
+template <typename T>
+__global__ void __launch_bounds__(256) k_input_r0(InputParams p) {
+  pdl_trigger();
+  pdl_wait();
+  const long long npix = (long long)p.S * p.H * p.W;
+  const long long HW = (long long)p.H * p.W;
+  const T* F = reinterpret_cast<const T*>(p.frame);
+  T* P = reinterpret_cast<T*>(p.P);
+  T* D = reinterpret_cast<T*>(p.delta);
+  const float eps = *p.eps;
+  const int C = p.C;
+  unsigned nact = 0;
+  bool bad = false;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < npix;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(q / HW);
+    float f[4], pv[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      f[c] = c < C ? ld(F + q * C + c) : 0.f;
+      pv[c] = c < C ? ld(P + q * C + c) : 0.f;
+    }
+    const bool first = p.first[s] != 0;
+    float mx = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      bad |= c < C && !isfinite(f[c]);
+      if (c < C) mx = fmaxf(mx, fabsf(f[c] - pv[c]));
+    }
+    const bool m = first || eps < 0.f || mx > eps;
+    p.mask[q] = m ? 1 : 0;
+    if (m) {
+      ++nact;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < C) {
+          st(D + q * p.Cp + c, first ? f[c] : f[c] - pv[c]);
+          st(P + q * C + c, f[c]);
+        }
+    }
+  }
+  if (bad) atomicOr(p.err, 1);
+  const int lane = threadIdx.x & 31;
+  unsigned n = (unsigned)warp_sum((int)nact);
+  warp_count_flush(p.n_active, lane, n);
+}
+
+void launch_input_r0(const InputParams& p, int dtype, cudaStream_t st) {
+  const long long npix = (long long)p.S * p.H * p.W;
+  long long blocks = (npix + 255) / 256;
+  const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
+  if (dtype == 1) launch_k(k_input_r0<__half>, dim3(grid), dim3(256), 0, st, 1, p);
+  else launch_k(k_input_r0<float>, dim3(grid), dim3(256), 0, st, 1, p);
+}
+
+// ---------------------------------------------------------------- a7, disjoint windows
+// thread = (output pixel, 8-channel chunk); lg_nch = log2(C / 8); window KK x KK.
+template <typename T, typename TC, int KK>
+__global__ void __launch_bounds__(256) k_maxpool_disj(PwParams p, int lg_nch) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int k = KK;
+  const int C = p.ep.C, nch = 1 << lg_nch;
+  const long long nout = (long long)p.S * p.H * p.W;
+  const long long HWo = (long long)p.H * p.W;
+  const T* din = reinterpret_cast<const T*>(p.in[0]);
+  T* dout = reinterpret_cast<T*>(p.ep.delta);
+  TC* A = reinterpret_cast<TC*>(p.poolA);
+  unsigned nact = 0;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < (nout << lg_nch);
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long q = g >> lg_nch;
+    const int j = (int)(g & (nch - 1));
+    const int s = (int)(q / HWo);
+    const int rem = (int)(q - (long long)s * HWo);
+    const int y = rem / p.W, x = rem - (rem / p.W) * p.W;
+    const long long ibase = ((long long)s * p.Hi + (long long)y * k) * p.Wi + (long long)x * k;
+    const bool first = p.ep.first[s] != 0;
+    // every load of the window at once: masks, deltas, accumulated inputs
+    uint8_t mk[KK * KK];
+    float d[KK * KK][8], a[KK * KK][8];
+#pragma unroll
+    for (int w = 0; w < KK * KK; ++w) {
+      const long long ip = ibase + (long long)(w / k) * p.Wi + (w % k);
+      mk[w] = p.min[0][ip];
+      ld8(din + ip * C + 8 * j, d[w]);
+      if (!first) ld8(A + ip * C + 8 * j, a[w]);
+    }
+    float mnew[8], mold[8];
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) mnew[c] = mold[c] = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < KK * KK; ++w) {
+      const bool on = first || mk[w];
+      any |= on;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float av = first ? 0.f : a[w][c];
+        const float dv = on ? d[w][c] : 0.f;             // select: a stale delta is never used
+        mnew[c] = fmaxf(mnew[c], av + dv);                // max_w(A + dx~)
+        mold[c] = fmaxf(mold[c], av);                     // max_w(A)
+        a[w][c] = av + dv;
+      }
+    }
+    if (j == 0) p.ep.mask[q] = any ? 1 : 0;
+    if (any) {
+      float o[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) o[c] = rnd<T>(first ? mnew[c] : mnew[c] - mold[c]);   // Eq. 3
+      st8(dout + q * C + 8 * j, o);
+      if (p.ep.O) {
+        float* O = p.ep.O + q * C + 8 * j;
+        float ov[8];
+        if (first) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) ov[c] = 0.f;
+        } else {
+          ld8(O, ov);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) ov[c] += o[c];
+        st8(O, ov);
+      }
+      if (j == 0) ++nact;
+      // A := A + dx~ on the active input pixels of the window (first frame: A := dx)
+#pragma unroll
+      for (int w = 0; w < KK * KK; ++w) {
+        if (first || mk[w]) st8(A + (ibase + (long long)(w / k) * p.Wi + (w % k)) * C + 8 * j, a[w]);
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31;
+  unsigned n = (unsigned)warp_sum((int)nact);
+  warp_count_flush(p.ep.n_active, lane, n);
+}
+
+// ---------------------------------------------------------------- a6, nearest upsample
+template <typename T>
+__global__ void __launch_bounds__(256) k_up_lean(PwParams p, int lg_nch) {
+  pdl_trigger();
+  pdl_wait();
+  const int C = p.ep.C, nch = 1 << lg_nch, f = p.up;
+  const long long nout = (long long)p.S * p.H * p.W;
+  const long long HWo = (long long)p.H * p.W;
+  const T* din = reinterpret_cast<const T*>(p.in[0]);
+  T* dout = reinterpret_cast<T*>(p.ep.delta);
+  unsigned nact = 0;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < (nout << lg_nch);
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long q = g >> lg_nch;
+    const int j = (int)(g & (nch - 1));
+    const int s = (int)(q / HWo);
+    const int rem = (int)(q - (long long)s * HWo);
+    const int y = rem / p.W, x = rem - (rem / p.W) * p.W;
+    const long long ip = ((long long)s * p.Hi + y / f) * p.Wi + x / f;
+    const uint8_t m = p.min[0][ip];
+    const uint4 v = *reinterpret_cast<const uint4*>(din + ip * C + 8 * j);   // with the mask
+    const bool on = p.ep.first[s] != 0 || m;
+    if (j == 0) p.ep.mask[q] = on ? 1 : 0;
+    if (on) {
+      *reinterpret_cast<uint4*>(dout + q * C + 8 * j) = v;
+      if (j == 0) ++nact;
+    }
+  }
+  const int lane = threadIdx.x & 31;
+  unsigned n = (unsigned)warp_sum((int)nact);
+  warp_count_flush(p.ep.n_active, lane, n);
+}
+
+static int lean_grid(long long items) {
+  long long blocks = (items + 255) / 256;
+  return (int)(blocks < 1 ? 1 : (blocks < 148 * 16 ? blocks : 148 * 16));
+}
+
+static int log2_exact(int v) {
+  int l = 0;
+  while ((1 << l) < v) ++l;
+  return (1 << l) == v ? l : -1;
+}
+
+bool lean_pool_ok(const PwParams& p, int dtype) {
+  return dtype == 1 && p.kind == 2 && p.k == 2 && p.stride == 2 && p.pad == 0 && p.Hi % p.k == 0 &&
+         p.Wi % p.k == 0 && p.ep.C % 8 == 0 && log2_exact(p.ep.C / 8) >= 0 && p.ep.act == 0;
+}
+
+bool lean_up_ok(const PwParams& p, int dtype) {
+  return dtype == 1 && p.kind == 4 && p.ep.C % 8 == 0 && log2_exact(p.ep.C / 8) >= 0 && p.ep.O == nullptr &&
+         p.ep.act == 0;
+}
+
+void launch_maxpool_disj(const PwParams& p, int cache32, cudaStream_t st) {
+  const int lg = log2_exact(p.ep.C / 8);
+  const int grid = lean_grid(((long long)p.S * p.H * p.W) << lg);
+  if (cache32) launch_k(k_maxpool_disj<__half, float, 2>, dim3(grid), dim3(256), 0, st, 1, p, lg);
+  else launch_k(k_maxpool_disj<__half, __half, 2>, dim3(grid), dim3(256), 0, st, 1, p, lg);
+}
+
+void launch_up_lean(const PwParams& p, cudaStream_t st) {
+  const int lg = log2_exact(p.ep.C / 8);
+  const int grid = lean_grid(((long long)p.S * p.H * p.W) << lg);
+  launch_k(k_up_lean<__half>, dim3(grid), dim3(256), 0, st, 1, p, lg);
+}
+
+}  // namespace dcnn

@@ -116,6 +116,13 @@ struct PwParams {
 void launch_pointwise(const PwParams& p, int dtype, int cache32, cudaStream_t st);
 void launch_pool_update(const PwParams& p, int dtype, int cache32, cudaStream_t st);
 
+// ---------------------------------------------------------------- latency-lean variants
+void launch_input_r0(const InputParams& p, int dtype, cudaStream_t st);   // radius 0, C <= 4
+bool lean_pool_ok(const PwParams& p, int dtype);       // 2x2 s2 max-pool, fp16, C/8 power of 2
+void launch_maxpool_disj(const PwParams& p, int cache32, cudaStream_t st);   // pool + A update
+bool lean_up_ok(const PwParams& p, int dtype);         // nearest upsample, fp16, C/8 power of 2
+void launch_up_lean(const PwParams& p, cudaStream_t st);
+
 // ---------------------------------------------------------------- control
 void launch_end_frame(uint8_t* first, long long* frame_idx, int S, cudaStream_t st);
 
