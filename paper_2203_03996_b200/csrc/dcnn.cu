@@ -167,7 +167,7 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
   static const int max_split = getenv("DCNN_TC_MAX_SPLIT") ? atoi(getenv("DCNN_TC_MAX_SPLIT")) : 8;
   // (down to N = 32 per CTA: a narrower slice shortens the epilogue of a tile, which is
   // what bounds a layer with few tiles)
-  while (ns0 < max_split && p.Np % (16 * ns0 * 2) == 0 && p.Np / (ns0 * 2) >= 32 && ntiles * ns0 * 2 <= 2 * 148) ns0 *= 2;
+  while (ns0 < max_split && p.Np % (16 * ns0 * 2) == 0 && p.Np / (ns0 * 2) >= 32 && ntiles * ns0 * 2 <= 148) ns0 *= 2;   // one wave
   while (p.Np / ns0 > 256) ns0 *= 2;            // one MMA N <= 256 per CTA
   if (p.Np % (16 * ns0)) return false;
   p.dbg = getenv("DCNN_TC_DBG") ? atoi(getenv("DCNN_TC_DBG")) : 0;
