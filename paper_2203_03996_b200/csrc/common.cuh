@@ -126,7 +126,21 @@ struct Epi {
   const uint8_t* first;        // [S] first-frame flag per stream
   long long HW;                // pixels per stream
   unsigned long long* n_active;  // counter: active output pixels (one atomic per warp)
+  // end-of-frame bookkeeping, done by the first kernel that runs after the input kernel
+  // (non-null for exactly one op): pend[s] := 0 and frame_idx[s] += 1 for every stream
+  uint8_t* pend_clear;
+  long long* frame_idx;
+  int n_streams;
 };
+
+// the end-of-frame bookkeeping of Epi::pend_clear; call after the PDL wait
+__device__ __forceinline__ void frame_bookkeeping(const Epi& e) {
+  if (e.pend_clear && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int s = 0; s < e.n_streams; ++s) {
+      e.pend_clear[s] = 0;
+      e.frame_idx[s] += 1;
+    }
+}
 
 constexpr int MAXK = 16;       // channels per lane in a warp epilogue: C <= 512
 

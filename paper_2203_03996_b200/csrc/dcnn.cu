@@ -92,7 +92,9 @@ struct dcnn_net {
   void* P = nullptr;
   void* in_delta = nullptr;
   uint8_t* in_mask = nullptr;
-  uint8_t* first = nullptr;
+  uint8_t* first = nullptr;         // [S] this frame's first-frame flags (written by the input kernel)
+  uint8_t* pend = nullptr;          // [S] first frame pending (create / dcnn_reset)
+  int bookkeeper = -1;              // op whose kernel clears pend and advances frame_idx
   long long* frame_idx = nullptr;
   int* err = nullptr;
   int* err_host = nullptr;          // pinned mirror, refreshed at the end of every frame
@@ -165,8 +167,9 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
   const int ntiles = S * ((o.H + 15) / 16) * ((o.W + 7) / 8);
   int ns0 = 1;
   static const int max_split = getenv("DCNN_TC_MAX_SPLIT") ? atoi(getenv("DCNN_TC_MAX_SPLIT")) : 8;
-  // (down to N = 32 per CTA: a narrower slice shortens the epilogue of a tile, which is
-  // what bounds a layer with few tiles)
+  // (never below N = 64 per CTA for parallelism alone: the MMA issue time of a tile does not
+  // shrink with N, and the cluster's max-norm exchange costs more than the shorter epilogue
+  // saves; all split CTAs must fit in one wave)
   while (ns0 < max_split && p.Np % (16 * ns0 * 2) == 0 && p.Np / (ns0 * 2) >= 32 && ntiles * ns0 * 2 <= 148) ns0 *= 2;   // one wave
   while (p.Np / ns0 > 256) ns0 *= 2;            // one MMA N <= 256 per CTA
   if (p.Np % (16 * ns0)) return false;
@@ -272,6 +275,9 @@ static Epi make_epi(dcnn_net* n, int i) {
   e.first = n->first;
   e.HW = (long long)o.H * o.W;
   e.n_active = n->stats + (size_t)(i + 1) * 8 + 1;
+  e.pend_clear = i == n->bookkeeper ? n->pend : nullptr;
+  e.frame_idx = n->frame_idx;
+  e.n_streams = n->S;
   return e;
 }
 
@@ -303,7 +309,7 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
   InputParams ip;
   ip.S = n->S; ip.H = n->inH; ip.W = n->inW; ip.C = n->inC; ip.Cp = n->inCp; ip.radius = n->radius;
   ip.frame = n->frame_in; ip.P = n->P; ip.delta = n->in_delta; ip.mask = n->in_mask;
-  ip.eps = n->eps; ip.first = n->first; ip.err = n->err; ip.n_active = n->stats + 1;
+  ip.eps = n->eps; ip.first = n->first; ip.pend = n->pend; ip.err = n->err; ip.n_active = n->stats + 1;
   {
     TimeScope ts(n, st, DCNN_KCLASS_INPUT);
     if (ip.radius == 0 && ip.C <= 4) launch_input_r0(ip, n->dtype, st);
@@ -434,8 +440,6 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
     cudaEventRecord(n->ev_join[k2 - 1], n->aux[k2 - 1]);
     cudaStreamWaitEvent(st, n->ev_join[k2 - 1], 0);
   }
-  launch_end_frame(n->first, n->frame_idx, n->S, st);
-  ++k;
   cudaMemcpyAsync(n->err_host, n->err, sizeof(int), cudaMemcpyDeviceToHost, st);
   if (kcount) *kcount = k;
 }
@@ -605,6 +609,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   CUDA_TRY(cudaMemset(n->in_delta, 0, in_px * n->inCp * es));
   if ((r = dalloc(n, &n->in_mask, in_px))) return r;
   if ((r = dalloc(n, &n->first, S))) return r;
+  if ((r = dalloc(n, &n->pend, S))) return r;
   if ((r = dalloc(n, &n->frame_idx, S * sizeof(long long)))) return r;
   if ((r = dalloc(n, &n->err, sizeof(int)))) return r;
   if ((r = dalloc(n, &n->eps, sizeof(float) * (L + 1)))) return r;
@@ -612,6 +617,12 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   n->n_counts = 2 * n_convs;
   if ((r = dalloc(n, &n->counts, sizeof(int) * std::max(1, n->n_counts)))) return r;
   CUDA_TRY(cudaMemset(n->first, 1, S));
+  CUDA_TRY(cudaMemset(n->pend, 1, S));
+  // end-of-frame bookkeeping rides on the first op that consumes the network input: its
+  // kernel runs after the input kernel has read the pending flags (PDL wait)
+  for (int i = 0; i < L && n->bookkeeper < 0; ++i)
+    for (int j = 0; j < n->ops[i].n_in; ++j)
+      if (n->ops[i].in[j] < 0) n->bookkeeper = i;
   CUDA_TRY(cudaMemset(n->frame_idx, 0, S * sizeof(long long)));
   CUDA_TRY(cudaMemset(n->err, 0, sizeof(int)));
   CUDA_TRY(cudaMemset(n->P, 0, n->frame_bytes));
@@ -793,8 +804,8 @@ dcnn_status dcnn_reset(dcnn_net* n, int32_t stream) {
   if (stream < -1 || stream >= n->S) return fail(DCNN_ERR_ARG, "stream index");
   CUDA_TRY(cudaSetDevice(n->device));
   cudaStream_t st = n->last ? n->last : n->cap;
-  if (stream < 0) CUDA_TRY(cudaMemsetAsync(n->first, 1, n->S, st));
-  else CUDA_TRY(cudaMemsetAsync(n->first + stream, 1, 1, st));
+  if (stream < 0) CUDA_TRY(cudaMemsetAsync(n->pend, 1, n->S, st));
+  else CUDA_TRY(cudaMemsetAsync(n->pend + stream, 1, 1, st));
   return DCNN_OK;
 }
 

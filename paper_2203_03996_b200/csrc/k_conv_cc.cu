@@ -100,6 +100,7 @@ template <typename T, typename TC, int ACT>
 __global__ void __launch_bounds__(CC_THREADS) k_conv_cc(ConvCCParams p) {
   pdl_trigger();
   pdl_wait();
+  frame_bookkeeping(p.ep);
   extern __shared__ __align__(16) unsigned char smem[];
   float* win = reinterpret_cast<float*>(smem);
   uint8_t* wmask = smem + ((size_t)p.WH * p.WW * p.CIC * sizeof(float) + 15) / 16 * 16;

@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   }
   // everything above overlapped the previous kernel (PDL); its outputs are needed now
   pdl_wait();
+  if (rank == 0) frame_bookkeeping(p.ep);
   TCTR(threadIdx.x == 0, 2);
   const int count = p.fused ? p.ntiles : *p.count;
   auto tile_of = [&](int ti) { return p.fused ? ti : p.list[ti]; };

@@ -37,7 +37,8 @@ __global__ void __launch_bounds__(256) k_input(InputParams p) {
     const int s = b / (tiles_y * tiles_x);
     const int ty = (b / tiles_x) % tiles_y;
     const int tx = b % tiles_x;
-    const bool first = p.first[s] != 0;
+    const bool first = p.pend[s] != 0;
+    if (ty == 0 && tx == 0 && tid == 0) p.first[s] = first ? 1 : 0;   // this frame's flag
     const float eps = *p.eps;
     const bool all = first || eps < 0.f;
     const int y0 = ty * IN_TS - r, x0 = tx * IN_TS - r;
@@ -107,20 +108,6 @@ void launch_input(const InputParams& p, int dtype, cudaStream_t st) {
   const int grid = tiles < 148 * 8 ? tiles : 148 * 8;
   if (dtype == 1) launch_k(k_input<__half>, dim3(grid), dim3(256), 0, st, 1, p);
   else launch_k(k_input<float>, dim3(grid), dim3(256), 0, st, 1, p);
-}
-
-// Clears the first-frame flags after the frame and advances frame counters.
-__global__ void k_end_frame(uint8_t* first, long long* frame_idx, int S) {
-  pdl_trigger();
-  pdl_wait();
-  for (int s = threadIdx.x; s < S; s += blockDim.x) {
-    first[s] = 0;
-    frame_idx[s] += 1;
-  }
-}
-
-void launch_end_frame(uint8_t* first, long long* frame_idx, int S, cudaStream_t st) {
-  launch_k(k_end_frame, dim3(1), dim3(128), 0, st, 1, first, frame_idx, S);
 }
 
 }  // namespace dcnn

@@ -41,7 +41,8 @@ __global__ void __launch_bounds__(256) k_input_r0(InputParams p) {
       f[c] = c < C ? ld(F + q * C + c) : 0.f;
       pv[c] = c < C ? ld(P + q * C + c) : 0.f;
     }
-    const bool first = p.first[s] != 0;
+    const bool first = p.pend[s] != 0;
+    if (q == (long long)s * HW) p.first[s] = first ? 1 : 0;        // this frame's flag
     float mx = 0.f;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -80,6 +81,7 @@ template <typename T, typename TC, int KK>
 __global__ void __launch_bounds__(256) k_maxpool_disj(PwParams p, int lg_nch) {
   pdl_trigger();
   pdl_wait();
+  frame_bookkeeping(p.ep);
   constexpr int k = KK;
   const int C = p.ep.C, nch = 1 << lg_nch;
   const long long nout = (long long)p.S * p.H * p.W;
@@ -161,6 +163,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_up_lean(PwParams p, int lg_nch) {
   pdl_trigger();
   pdl_wait();
+  frame_bookkeeping(p.ep);
   const int C = p.ep.C, nch = 1 << lg_nch, f = p.up;
   const long long nout = (long long)p.S * p.H * p.W;
   const long long HWo = (long long)p.H * p.W;

@@ -183,6 +183,7 @@ template <typename T, typename TC, int KIND, int ACT>
 __global__ void __launch_bounds__(256) k_pointwise(PwParams p) {
   pdl_trigger();
   pdl_wait();
+  frame_bookkeeping(p.ep);
   const int lane = threadIdx.x & 31;
   const long long npix = (long long)p.S * p.H * p.W;
   const long long HWo = (long long)p.H * p.W;

@@ -21,7 +21,8 @@ struct InputParams {
   void* delta;                  // [S,H,W,C] T
   uint8_t* mask;                // [S,H,W]
   const float* eps;             // device slot of eps_in
-  const uint8_t* first;         // [S]
+  uint8_t* first;               // [S] out: this frame's first-frame flags (copied from pend)
+  const uint8_t* pend;          // [S] first-frame pending (set at create / by dcnn_reset)
   int* err;                     // sticky error word (bit 0: non-finite input)
   unsigned long long* n_active;
 };
@@ -124,6 +125,5 @@ bool lean_up_ok(const PwParams& p, int dtype);         // nearest upsample, fp16
 void launch_up_lean(const PwParams& p, cudaStream_t st);
 
 // ---------------------------------------------------------------- control
-void launch_end_frame(uint8_t* first, long long* frame_idx, int S, cudaStream_t st);
 
 }  // namespace dcnn
