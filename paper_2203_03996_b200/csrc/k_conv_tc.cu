@@ -236,12 +236,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       __syncwarp();                            // previous use of hm / info bits finished
       {
         int hy = hy_0, hx = hx_0;              // (hy, hx) of px = lane, advanced incrementally
-        for (int px = lane; px < npx; px += 32) {
-          const int iy = iy0 + hy, ix = ix0 + hx;
-          hm[px] = (iy >= 0 && iy < p.H && ix >= 0 && ix < p.W) ? mi[iy * p.W + ix] : 0;
-          hx += dx32;
-          hy += dy32;
-          if (hx >= p.WW) { hx -= p.WW; ++hy; }
+        for (int px0 = lane; px0 < npx; px0 += 32 * 8) {
+          uint8_t v[8];                        // 8 loads in flight per lane, then 8 smem stores
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int iy = iy0 + hy, ix = ix0 + hx;
+            v[k] = (px0 + 32 * k < npx && iy >= 0 && iy < p.H && ix >= 0 && ix < p.W) ? mi[iy * p.W + ix] : 0;
+            hx += dx32;
+            hy += dy32;
+            if (hx >= p.WW) { hx -= p.WW; ++hy; }
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (px0 + 32 * k < npx) hm[px0 + 32 * k] = v[k];
         }
       }
       __syncwarp();
@@ -568,14 +575,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       auto stage_move = [&](unsigned char* area, __half* base, int n16, uint32_t pm, int dir, uint32_t zm = 0u) {
         const int lg = n16 > 2 ? 2 : n16 - 1, lp = 1 << lg;
         __syncwarp();
-#pragma unroll 1
-        for (int i = 0; i < lp; ++i) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i >= lp) break;
           const int pl = (i << (5 - lg)) + (lane >> lg), c = lane & (lp - 1);
           if (c < n16 && ((pm >> pl) & 1u)) {
             uint4* g = reinterpret_cast<uint4*>(base + (pixw + (long long)(pl >> 3) * p.Wo + (pl & 7)) * Cg + c * 8);
             uint4* sm = reinterpret_cast<uint4*>(area + pl * 80 + c * 16);
             if (dir) *g = ((zm >> pl) & 1u) ? make_uint4(0u, 0u, 0u, 0u) : *sm;
             else *sm = *g;
+          }
+        }
+        __syncwarp();
+      };
+      // fill SA / ST with the x^A / x^T rows of the pixels in pm: every global load of both
+      // areas is issued before the first shared store (one round trip, not eight)
+      auto stage_fill2 = [&](const __half* baseA, const __half* baseT, int n16, uint32_t pm) {
+        const int lg = n16 > 2 ? 2 : n16 - 1, lp = 1 << lg;
+        uint4 va[4], vt[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int pl = (i << (5 - lg)) + (lane >> lg), c = lane & (lp - 1);
+          if (i < lp && c < n16 && ((pm >> pl) & 1u)) {
+            const long long off = (pixw + (long long)(pl >> 3) * p.Wo + (pl & 7)) * Cg + c * 8;
+            va[i] = *reinterpret_cast<const uint4*>(baseA + off);
+            vt[i] = *reinterpret_cast<const uint4*>(baseT + off);
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int pl = (i << (5 - lg)) + (lane >> lg), c = lane & (lp - 1);
+          if (i < lp && c < n16 && ((pm >> pl) & 1u)) {
+            *reinterpret_cast<uint4*>(SA + pl * 80 + c * 16) = va[i];
+            *reinterpret_cast<uint4*>(ST + pl * 80 + c * 16) = vt[i];
           }
         }
         __syncwarp();
@@ -588,10 +621,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       auto n16_of = [&](int sl) { return C - sl >= 32 ? 4 : (C - sl) / 8; };
       const bool need_cache = trunc && !first;
       // ---- loads that do not depend on the accumulator: the first slice of the cache rows
-      if (need_cache && coal && actm && C > 0) {
-        stage_move(SA, gA, n16_of(0), actm, 0);
-        stage_move(ST, gT, n16_of(0), actm, 0);
-      }
+      if (need_cache && coal && actm && C > 0) stage_fill2(gA, gT, n16_of(0), actm);
       if (act && O && !first)
         for (int c = 0; c < C; c += 32) prefetch_l2(O + c);
       const int acc = u & 1;
@@ -632,10 +662,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         float mx = 0.f;
 #pragma unroll 1
         for (int c0 = 0; c0 < C; c0 += 8) {
-          if (coal && need_cache && actm && c0 > 0 && (c0 & 31) == 0) {   // next slice
-            stage_move(SA, gA + c0, n16_of(c0), actm, 0);
-            stage_move(ST, gT + c0, n16_of(c0), actm, 0);
-          }
+          if (coal && need_cache && actm && c0 > 0 && (c0 & 31) == 0)     // next slice
+            stage_fill2(gA + c0, gT + c0, n16_of(c0), actm);
           float z[8], a[8], t[8];
           chunk_in(c0, z, a, t);
           if (act) {
@@ -688,10 +716,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 #pragma unroll 1
       for (int c0 = single ? (C - 1) & ~7 : 0; c0 < C; c0 += 8) {
         if (single) goto flush;                  // results already staged by pass 1
-        if (coal && need_cache && actm && (c0 & 31) == 0 && (c0 > 0 || C > 32)) {   // reload the slice
-          stage_move(SA, gA + c0, n16_of(c0), actm, 0);
-          stage_move(ST, gT + c0, n16_of(c0), actm, 0);
-        }
+        if (coal && need_cache && actm && (c0 & 31) == 0 && (c0 > 0 || C > 32))     // reload the slice
+          stage_fill2(gA + c0, gT + c0, n16_of(c0), actm);
         float z[8], a[8], t[8], o[8];
         chunk_in(c0, z, a, t);
         if (act) {
