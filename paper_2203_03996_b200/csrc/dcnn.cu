@@ -712,6 +712,12 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         if ((r = dalloc(n, &o.wtc, w.size() * 2))) return r;
         CUDA_TRY(cudaMemcpy(o.wtc, w.data(), w.size() * 2, cudaMemcpyHostToDevice));
         p.wtc = o.wtc;
+        // pending-residual flags (x^T != 0) for truncating layers on the coalesced fp16 path
+        if (o.act != DCNN_ACT_NONE && !n->cache32 && o.C % 8 == 0 && !(n->flags & DCNN_FLAG_HYBRID_DISPATCH)) {
+          if ((r = dalloc(n, &p.tflag, S * o.H * o.W))) return r;
+          CUDA_TRY(cudaMemset(p.tflag, 0, S * o.H * o.W));
+          CUDA_TRY(cudaMemset(o.xT, 0, S * o.H * o.W * o.C * n->cesz));   // flag 0 <=> x^T == 0
+        }
         // TMA view of the input delta [S][Hi][Wi][Ci] fp16: dims (C, x, y, stream); a box is
         // 8 channels x one stride phase of the halo columns x all halo rows
         {

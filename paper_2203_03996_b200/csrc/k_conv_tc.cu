@@ -590,26 +590,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       };
       // fill SA / ST with the x^A / x^T rows of the pixels in pm: every global load of both
       // areas is issued before the first shared store (one round trip, not eight)
-      auto stage_fill2 = [&](const __half* baseA, const __half* baseT, int n16, uint32_t pm) {
+      auto stage_fill2 = [&](const __half* baseA, const __half* baseT, int n16, uint32_t pm, uint32_t pmt) {
         const int lg = n16 > 2 ? 2 : n16 - 1, lp = 1 << lg;
         uint4 va[4], vt[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int pl = (i << (5 - lg)) + (lane >> lg), c = lane & (lp - 1);
-          if (i < lp && c < n16 && ((pm >> pl) & 1u)) {
-            const long long off = (pixw + (long long)(pl >> 3) * p.Wo + (pl & 7)) * Cg + c * 8;
-            va[i] = *reinterpret_cast<const uint4*>(baseA + off);
-            vt[i] = *reinterpret_cast<const uint4*>(baseT + off);
-          }
+          const long long off = (pixw + (long long)(pl >> 3) * p.Wo + (pl & 7)) * Cg + c * 8;
+          if (i < lp && c < n16 && ((pm >> pl) & 1u)) va[i] = *reinterpret_cast<const uint4*>(baseA + off);
+          if (i < lp && c < n16 && ((pmt >> pl) & 1u)) vt[i] = *reinterpret_cast<const uint4*>(baseT + off);
         }
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int pl = (i << (5 - lg)) + (lane >> lg), c = lane & (lp - 1);
-          if (i < lp && c < n16 && ((pm >> pl) & 1u)) {
-            *reinterpret_cast<uint4*>(SA + pl * 80 + c * 16) = va[i];
-            *reinterpret_cast<uint4*>(ST + pl * 80 + c * 16) = vt[i];
-          }
+          if (i < lp && c < n16 && ((pm >> pl) & 1u)) *reinterpret_cast<uint4*>(SA + pl * 80 + c * 16) = va[i];
+          if (i < lp && c < n16 && ((pmt >> pl) & 1u)) *reinterpret_cast<uint4*>(ST + pl * 80 + c * 16) = vt[i];
         }
         __syncwarp();
       };
@@ -620,8 +616,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       __half* gD = reinterpret_cast<__half*>(e.delta) + chan0;
       auto n16_of = [&](int sl) { return C - sl >= 32 ? 4 : (C - sl) / 8; };
       const bool need_cache = trunc && !first;
+      // pixels whose x^T may be non-zero (all active ones without the pending-residual flags)
+      const bool tpend = act && (p.tflag == nullptr || p.tflag[pix] != 0);
+      const uint32_t tm = __ballot_sync(0xffffffffu, tpend);
       // ---- loads that do not depend on the accumulator: the first slice of the cache rows
-      if (need_cache && coal && actm && C > 0) stage_fill2(gA, gT, n16_of(0), actm);
+      if (need_cache && coal && actm && C > 0) stage_fill2(gA, gT, n16_of(0), actm, tm);
       if (act && O && !first)
         for (int c = 0; c < C; c += 32) prefetch_l2(O + c);
       const int acc = u & 1;
@@ -646,7 +645,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         if (coal) {
           const int off = lane * 80 + (c0 & 31) * 2;
           unpack8<__half>(*reinterpret_cast<const uint4*>(SA + off), a);
-          unpack8<__half>(*reinterpret_cast<const uint4*>(ST + off), t);
+          if (tpend) unpack8<__half>(*reinterpret_cast<const uint4*>(ST + off), t);   // else x^T = 0
         } else {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
@@ -663,7 +662,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 #pragma unroll 1
         for (int c0 = 0; c0 < C; c0 += 8) {
           if (coal && need_cache && actm && c0 > 0 && (c0 & 31) == 0)     // next slice
-            stage_fill2(gA + c0, gT + c0, n16_of(c0), actm);
+            stage_fill2(gA + c0, gT + c0, n16_of(c0), actm, tm);
           float z[8], a[8], t[8];
           chunk_in(c0, z, a, t);
           if (act) {
@@ -717,7 +716,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       for (int c0 = single ? (C - 1) & ~7 : 0; c0 < C; c0 += 8) {
         if (single) goto flush;                  // results already staged by pass 1
         if (coal && need_cache && actm && (c0 & 31) == 0 && (c0 > 0 || C > 32))     // reload the slice
-          stage_fill2(gA + c0, gT + c0, n16_of(c0), actm);
+          stage_fill2(gA + c0, gT + c0, n16_of(c0), actm, tm);
         float z[8], a[8], t[8], o[8];
         chunk_in(c0, z, a, t);
         if (act) {
@@ -771,7 +770,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           if (trunc) {
             stage_move(SA, gA + sl, n16, updm, 1);
             TCTR(tid == 0 && u == 0 && sl == 0, 20);
-            stage_move(ST, gT + sl, n16, actm, 1, updm);   // x^T := 0 where updated
+            // x^T := x^T + dx where truncated; := 0 where updated and it was pending
+            stage_move(ST, gT + sl, n16, (actm & ~updm) | (updm & tm), 1, updm);
           }
           TCTR(tid == 0 && u == 0 && sl == 0, 21);
           stage_move(SD, gD + sl, n16, updm, 1);
@@ -804,6 +804,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       }
       TCTR(tid == 0 && u == 0, 17);
       if (inb && rank == 0 && half == 0) e.mask[pix] = upd ? 1 : 0;   // final mask of every tile pixel
+      // pending-residual flag: written by one thread per pixel after every CTA of the cluster
+      // and both halves have read it (they all passed the max-norm exchange)
+      if (trunc && p.tflag && act && rank == 0 && half == 0 && upd == tpend) p.tflag[pix] = upd ? 0 : 1;
       nact += (upd && rank == 0 && half == 0) ? 1 : 0;
       TCTR(tid == 0 && u == 0, 12);
       tc::tc_fence_before();

@@ -87,6 +87,8 @@ struct ConvTCParams {
   int fused;                    // 1: iterate all tiles, decide activity in-kernel (no a2 launch)
   int ntiles;                   // S*nty*ntx (fused mode)
   unsigned long long* tstats;   // fused mode: [.., tiles_total, skip, sparse, dense, m_conv px]
+  uint8_t* tflag;               // [S,Ho,Wo] x^T != 0 ("pending residual") or null: x^T is then
+                                // read only where flagged and written only when it changes
   const __half* delta_in;
   const uint8_t* mask_in;
   const __half* wtc;            // [nsplit][ncb*kh*kw][BK/8][Ns][8] fp16 (smem image of each step)
