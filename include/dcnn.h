@@ -196,6 +196,13 @@ DCNN_API dcnn_status dcnn_enable_kernel_timing(dcnn_net* net, int32_t class_mask
 DCNN_API dcnn_status dcnn_kernel_timing(dcnn_net* net, int32_t kernel_class, float* ms,
                                         int32_t* launches);
 
+/* Per-launch device times of the most recent frame (profiling; needs
+ * dcnn_enable_kernel_timing): for up to max timed launches, in capture order, the op
+ * index (-1 = input layer), kernel class and milliseconds.  *count receives the total
+ * number of timed launches.  Synchronises the device. */
+DCNN_API dcnn_status dcnn_debug_launch_times(dcnn_net* net, int32_t max, int32_t* op, int32_t* cls, float* ms,
+                                             int32_t* count);
+
 /* Debug poisoning: fill every delta buffer with NaN so
  * that any read of a masked-off (stale) value would surface in the outputs. */
 DCNN_API dcnn_status dcnn_debug_poison(dcnn_net* net);

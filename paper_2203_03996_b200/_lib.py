@@ -82,10 +82,11 @@ def load_library(path: str = LIB_PATH):
     lib.dcnn_kernel_timing.argtypes = [vp, C.c_int32, C.POINTER(C.c_float), C.POINTER(C.c_int32)]
     lib.dcnn_debug_poison.argtypes = [vp]
     lib.dcnn_debug_tc_trace.argtypes = [vp]
+    lib.dcnn_debug_launch_times.argtypes = [vp, C.c_int32, vp, vp, vp, C.POINTER(C.c_int32)]
     for name in ["dcnn_create_net", "dcnn_set_threshold", "dcnn_process_frame",
                  "dcnn_process_frame_host", "dcnn_reset", "dcnn_op_shape", "dcnn_get_stats",
                  "dcnn_debug_read", "dcnn_enable_kernel_timing", "dcnn_kernel_timing",
-                 "dcnn_debug_poison", "dcnn_debug_tc_trace"]:
+                 "dcnn_debug_poison", "dcnn_debug_tc_trace", "dcnn_debug_launch_times"]:
         getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -234,6 +235,17 @@ class DeltaNet:
         ms, n = C.c_float(), C.c_int32()
         _check(self.lib, self.lib.dcnn_kernel_timing(self.h, kclass, C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+    def launch_times(self):
+        """[(op, kernel class, ms)] of every timed launch of the latest frame."""
+        n = C.c_int32(0)
+        _check(self.lib, self.lib.dcnn_debug_launch_times(self.h, 0, None, None, None, C.byref(n)))
+        op = np.zeros(n.value, np.int32)
+        cl = np.zeros(n.value, np.int32)
+        ms = np.zeros(n.value, np.float32)
+        _check(self.lib, self.lib.dcnn_debug_launch_times(self.h, n.value, op.ctypes.data, cl.ctypes.data,
+                                                          ms.ctypes.data, C.byref(n)))
+        return list(zip(op.tolist(), cl.tolist(), ms.tolist()))
 
     def debug_poison(self):
         _check(self.lib, self.lib.dcnn_debug_poison(self.h))

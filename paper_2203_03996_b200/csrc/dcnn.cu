@@ -119,7 +119,7 @@ struct dcnn_net {
   cudaEvent_t ev_fork = nullptr, ev_input = nullptr;
   // kernel timing (profiling)
   int timing_mask = 0;
-  struct Timed { int cls; cudaEvent_t a, b; };
+  struct Timed { int cls, op; cudaEvent_t a, b; };
   std::vector<Timed> timed;
 };
 
@@ -242,13 +242,19 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
       const auto pa = a_bytes_of(BK);
       if (pa.first >> 4 >= (1 << 14)) continue;                       // LBO field
       const int Ns = p.Np / ns0;
+      const int ncb = o.Ci / BK;
       for (int tg = ntaps; tg >= 1; --tg) {
         if (ntaps % tg) continue;
         const size_t b_bytes = (size_t)tg * Ns * BK * 2;
         if (2 * (size_t)pa.second + (size_t)min_stages * b_bytes > budget) continue;
-        int stages = (int)((budget - 2 * (size_t)pa.second) / b_bytes);
+        // up to 4 halo buffers (one per channel block in flight) while >= min_stages weight
+        // stages still fit: with 2 buffers a block's TMA only starts when the MMAs of the block
+        // two back retire, so multi-block layers would wait on TMA latency
+        int nab = 2;
+        while (nab < 4 && nab < ncb && (size_t)(nab + 1) * pa.second + (size_t)min_stages * b_bytes <= budget) ++nab;
+        int stages = (int)((budget - (size_t)nab * pa.second) / b_bytes);
         if (stages > 16) stages = 16;
-        set_common(ns0, BK, tg, stages, 2, 0);
+        set_common(ns0, BK, tg, stages, nab, 0);
         return true;
       }
     }
@@ -286,10 +292,11 @@ struct TimeScope {
   dcnn_net* n;
   cudaStream_t st;
   int idx = -1;
-  TimeScope(dcnn_net* n_, cudaStream_t st_, int cls) : n(n_), st(st_) {
+  TimeScope(dcnn_net* n_, cudaStream_t st_, int cls, int op = -1) : n(n_), st(st_) {
     if (!(n->timing_mask & cls)) return;
     dcnn_net::Timed t;
     t.cls = cls;
+    t.op = op;
     cudaEventCreate(&t.a);
     cudaEventCreate(&t.b);
     idx = (int)n->timed.size();
@@ -367,7 +374,7 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       tp.stats = n->stats + (size_t)(i + 1) * 8;
       const bool fused = o.tc && !(n->flags & DCNN_FLAG_HYBRID_DISPATCH);
       if (!fused) {                    // tensor-core convs decide their tiles in-kernel
-        TimeScope ts(n, ost, DCNN_KCLASS_TILES);
+        TimeScope ts(n, ost, DCNN_KCLASS_TILES, i);
         launch_tiles(tp, ost);
         ++k;
       }
@@ -384,7 +391,7 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       cp.G = group_lanes(o.C);
       cp.ep = make_epi(n, i);
       if (!o.tc || (n->flags & DCNN_FLAG_HYBRID_DISPATCH)) {
-        TimeScope ts(n, ost, DCNN_KCLASS_CONV);
+        TimeScope ts(n, ost, DCNN_KCLASS_CONV, i);
         launch_conv_cc(cp, n->dtype, n->cache32, o.grid_cc, ost);
         ++k;
       }
@@ -398,7 +405,7 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
         p.ntiles = n->S * o.nty * o.ntx;
         p.tstats = n->stats + (size_t)(i + 1) * 8;
         p.ep = make_epi(n, i);
-        TimeScope ts(n, ost, DCNN_KCLASS_CONV);
+        TimeScope ts(n, ost, DCNN_KCLASS_CONV, i);
         launch_conv_tc(p, n->cache32, o.grid_tc, ost);
         ++k;
       }
@@ -422,14 +429,14 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       pp.ep = make_epi(n, i);
       const bool lean_pool = lean_pool_ok(pp, n->dtype);
       {
-        TimeScope ts(n, ost, DCNN_KCLASS_POINTWISE);
+        TimeScope ts(n, ost, DCNN_KCLASS_POINTWISE, i);
         if (lean_pool) launch_maxpool_disj(pp, n->cache32, ost);       // pool + A update, one launch
         else if (lean_up_ok(pp, n->dtype)) launch_up_lean(pp, ost);
         else launch_pointwise(pp, n->dtype, n->cache32, ost);
       }
       ++k;
       if (o.kind == DCNN_OP_MAXPOOL && !lean_pool) {
-        TimeScope ts(n, ost, DCNN_KCLASS_POINTWISE);
+        TimeScope ts(n, ost, DCNN_KCLASS_POINTWISE, i);
         launch_pool_update(pp, n->dtype, n->cache32, ost);
         ++k;
       }
@@ -975,6 +982,26 @@ dcnn_status dcnn_kernel_timing(dcnn_net* n, int32_t cls, float* ms, int32_t* lau
   }
   *ms = tot;
   *launches = cnt;
+  return DCNN_OK;
+}
+
+dcnn_status dcnn_debug_launch_times(dcnn_net* n, int32_t max, int32_t* op, int32_t* cls, float* ms,
+                                     int32_t* count) {
+  if (!n || !count) return fail(DCNN_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(n->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  int k = 0;
+  for (auto& t : n->timed) {
+    if (k < max) {
+      float e = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&e, t.a, t.b));
+      if (op) op[k] = t.op;
+      if (cls) cls[k] = t.cls;
+      if (ms) ms[k] = e;
+    }
+    ++k;
+  }
+  *count = k;
   return DCNN_OK;
 }
 

@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       const uint8_t* hm = smem + L.hmask + pg_slot * TC_HMASK_BYTES;
       unsigned char* A = smem + L.a0 + b * p.a_bytes;
       int hy = hy_0, hx = hx_0;
-      for (int px = lt; px < npx; px += 32) {
+      for (int px = (p.dbg & 8) ? npx : lt; px < npx; px += 32) {   // dbg 8: no zero pass (timing only)
         const int iy = pg_iy0 + hy, ix = pg_ix0 + hx;
         if (!hm[px] && iy >= 0 && iy < p.H && ix >= 0 && ix < p.W) {
           unsigned char* d = A + (hx & lgs) * p.phase_bytes + (hy * p.WQ + (hx >> lgs)) * 16;
@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         const int s = tile / (p.nty * p.ntx);
         const int ty = (tile / p.ntx) % p.nty, tx = tile % p.ntx;
         const int iy0 = ty * 16 * p.stride - p.pad, ix0 = tx * 8 * p.stride - p.pad;
+        if (p.dbg & 16) { tc::mbar_arrive(&a_tma[b]); return; }   // dbg 16: no halo copies (timing only)
         tc::mbar_arrive_expect_tx(&a_tma[b], gbytes);
         const uint32_t A = tc::smem_u32(smem + L.a0 + b * p.a_bytes);
         // one box of 8 channels x (columns of one stride phase) x halo rows per plane
@@ -480,6 +481,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         tc::mbar_wait(&a_full[b], (k / NA) & 1);
         tc::tc_fence_after();
         TCTR(lane == 0 && k == 0, 7);
+        TCTR(lane == 0 && k >= 1 && k <= 3, 24 + k);   // 25..27: halo block k ready for the MMAs
         const uint32_t abase = tc::smem_u32(smem + L.a0 + b * p.a_bytes);
         for (int g = 0; g < ngroups; ++g, ++j) {
           const int stp = cb * ngroups + g;
@@ -487,6 +489,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           tc::mbar_wait(&b_full[st], p.resident ? 0 : (j / p.stages) & 1);
           tc::tc_fence_after();
           TCTR(lane == 0 && j == 0, 8);
+          TCTR(lane == 0 && (j == 3 || j == 6 || j == 9 || j == 11), j == 3 ? 28 : j == 6 ? 29 : j == 9 ? 30 : 31);
           const uint32_t bbase = tc::smem_u32(bstage + (size_t)st * p.b_bytes);
           if (tc::elect_one()) {
             // all MMAs of tg taps x BK/16 K-steps against one weight step
@@ -501,7 +504,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                 bd += b_step;                    // + 2 core-matrix chunks (B)
               }
             }
-            if (!p.resident) tc::mma_commit(&b_empty[st]);   // stage reusable once these finish
+            if (!p.resident) {
+              if (p.dbg & 64) tc::mbar_arrive(&b_empty[st]);   // dbg 64: release early (timing only)
+              else tc::mma_commit(&b_empty[st]);               // stage reusable once these finish
+            }
           }
           __syncwarp();
           TCTR(lane == 0 && j == 0, 24);

@@ -8,9 +8,10 @@ from paper_2203_03996_b200 import DeltaNet
 from paper_2203_03996_b200._lib import debug_tc_trace
 NAMES = ["start", "setup", "pdl_wait", "mask0", "pub0", "halo_iss0", "loaders_done", "halo_land0",
          "w_land0", "mma0_commit", "epi_wait0", "epi_acc0", "epi_done0", "roles_done", "final_sync", "epi_pass1", "epi_norm",
-         "epi_pass2", "epi_flush", "p2_chunks", "p2_flushA", "p2_flushT", "p2_flushD", "-", "mma_grp0"]
+         "epi_pass2", "epi_flush", "p2_chunks", "p2_flushA", "p2_flushT", "p2_flushD", "-", "mma_grp0", "a1", "a2", "a3", "w3", "w6", "w9", "w11"]
 if __name__ == "__main__":
-    cfgs = [(16, 8, 64, 64, 3, 1), (128, 128, 64, 64, 3, 1), (20, 20, 512, 512, 3, 1), (160, 160, 64, 64, 3, 1)]
+    cfgs = [tuple(map(int, a.split(','))) for a in sys.argv[1:]] or [(16, 8, 64, 64, 3, 1), (128, 128, 64, 64, 3, 1),
+                                                                   (20, 20, 512, 512, 3, 1), (160, 160, 64, 64, 3, 1)]
     for (H, W, ci, co, k, s) in cfgs:
         b = nets._Builder("c", H, W, ci, 0, "f16")
         i = b.conv(-1, co, k, stride=s, act="relu")
