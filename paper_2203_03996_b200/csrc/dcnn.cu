@@ -156,23 +156,27 @@ static dcnn_status plan_cc(Op& o) {
   return DCNN_OK;
 }
 
+// Plan of the tcgen05 conv of one layer.  Every candidate (output-channel split over a
+// cluster, input-channel block BK, resident or streamed weights, taps per weight step,
+// halo buffers) that fits the shared-memory budget is scored with a small latency model
+// (measured on B200 with tools/trace_tc.py; µs):
+//   one MMA (M128 x N x K16)       0.05 for N <= 128, 0.075 for N = 256 (issue-bound)
+//   one halo block (TMA + zero)    1.5 latency; NA buffers keep NA - 1 blocks in flight
+//   one streamed weight step       0.55 + bytes / 40 kB-per-µs (throughput-bound: a deeper ring
+//                                  does not hide it; ~40 GB/s of bulk copies per SM)
+//   epilogue of a tile             3.5 for <= 32 channels per thread (single pass), + 0.35 per
+//                                  further channel (two passes), + 1.0 for the DSMEM exchange
+// and the cheapest one is taken: tile latency = max(halo pipeline, weight pipeline, MMAs)
+// + epilogue, plus the extra tiles a CTA runs when the tiles exceed one wave.
 static bool plan_tc(Op& o, int dtype, int flags, int S) {
   if (dtype != DCNN_F16 || (flags & DCNN_FLAG_NO_TENSOR_CORES)) return false;
   if (o.Ci % 16 || o.C > 512) return false;
   ConvTCParams& p = o.tcp;
   memset(&p, 0, sizeof(p));
   p.Np = (o.C + 15) / 16 * 16;
-  // split output channels over a cluster when the layer has few tiles (small maps,
-  // wide layers): every CTA then streams only its slice of the weights
   const int ntiles = S * ((o.H + 15) / 16) * ((o.W + 7) / 8);
-  int ns0 = 1;
   static const int max_split = getenv("DCNN_TC_MAX_SPLIT") ? atoi(getenv("DCNN_TC_MAX_SPLIT")) : 8;
-  // (never below N = 64 per CTA for parallelism alone: the MMA issue time of a tile does not
-  // shrink with N, and the cluster's max-norm exchange costs more than the shorter epilogue
-  // saves; all split CTAs must fit in one wave)
-  while (ns0 < max_split && p.Np % (16 * ns0 * 2) == 0 && p.Np / (ns0 * 2) >= 32 && ntiles * ns0 * 2 <= 148) ns0 *= 2;   // one wave
-  while (p.Np / ns0 > 256) ns0 *= 2;            // one MMA N <= 256 per CTA
-  if (p.Np % (16 * ns0)) return false;
+  static const bool no_resident = getenv("DCNN_TC_NO_RESIDENT") != nullptr;
   p.dbg = getenv("DCNN_TC_DBG") ? atoi(getenv("DCNN_TC_DBG")) : 0;
   const int s = o.stride, d = o.dil;
   if (s > 2 || o.kh * o.kw > 64) return false;         // stride phases / tap table
@@ -180,85 +184,83 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
   p.WW = 7 * s + (o.kw - 1) * d + 1;
   if (p.HH * p.WW > 1024 || p.HH > 64 || p.WW > 32) return false;   // halo mask buffer, row bit masks
   p.WQ = (p.WW + s - 1) / s;
-  // fixed part of the layout (barriers, tile ring, halo masks): see tc_layout()
-  const size_t budget = 226 * 1024 - 69632;
+  // fixed part of the layout (barriers, tile ring, halo masks, epilogue staging): tc_layout()
+  const double budget = 226 * 1024 - 69632;
   const int ntaps = o.kh * o.kw;
-  // halo buffer = [stride phase][8-channel plane][halo row][column of the phase][8 ch];
-  // every plane is one TMA box (128-B aligned), its byte size is the A-operand LBO
-  auto a_bytes_of = [&](int BK) {
-    const int plane = (p.HH * p.WQ * 16 + 127) / 128 * 128;
-    const int phase = (BK / 8) * plane;
-    return std::make_pair(plane, s * phase);
-  };
-  auto set_common = [&](int ns, int BK, int tg, int stages, int nab, int resident) {
-    p.nsplit = ns;
-    p.Ns = p.Np / ns;
-    p.BK = BK;
-    p.ncb = o.Ci / BK;
-    auto pa = a_bytes_of(BK);
-    p.plane = pa.first;
-    p.phase_bytes = (BK / 8) * pa.first;
-    p.a_bytes = pa.second;
-    p.tg = tg;
-    p.b_bytes = tg * p.Ns * BK * 2;
-    p.stages = stages;
-    p.n_abuf = nab;
-    p.resident = resident;
-    p.n_acc = 2;
-    p.acc_stride = (p.Ns + 31) / 32 * 32;
-    int tc = 32;
-    while (tc < 2 * p.acc_stride) tc *= 2;
-    p.tmem_cols = tc;
-  };
-  static const bool no_resident = getenv("DCNN_TC_NO_RESIDENT") != nullptr;
-  // 1. resident weights: the CTA's whole weight slice sits in smem next to >= 2 halo
-  //    buffers (loaded once per kernel, before the PDL wait); allow up to 4x more
-  //    channel splitting than parallelism alone asks for to get there
-  for (int ns = ns0; !no_resident && ns <= 8 && ns <= 4 * ns0; ns *= 2) {
-    if (p.Np % (16 * ns) || p.Np / ns < 16) break;
+  const int plane = (p.HH * p.WQ * 16 + 127) / 128 * 128;
+  struct Cand { double cost; int ns, BK, tg, stages, nab, resident; };
+  Cand best = {1e30, 0, 0, 0, 0, 0, 0};
+  for (int ns = 1; ns <= max_split; ns *= 2) {
+    if (p.Np % (16 * ns) || p.Np / ns < 16 || p.Np / ns > 256) continue;
+    if (ns > 1 && ntiles * ns > 148) continue;         // all split CTAs in one wave
     const int Ns = p.Np / ns;
+    const double t_mma = Ns <= 128 ? 0.05 : 0.075;
+    const int waves = (ntiles * ns + 147) / 148;
+    const int c_thread = (Ns + 31) / 32 * 16;            // channels of an epilogue thread
+    const double t_epi = 3.5 + 0.35 * std::max(0, c_thread - 32) + (ns > 1 ? 1.0 : 0.0);
     for (int BK = 64; BK >= 16; BK /= 2) {
       if (o.Ci % BK) continue;
-      const auto pa = a_bytes_of(BK);
-      if (pa.first >> 4 >= (1 << 14)) continue;                       // LBO field
-      const size_t wbytes = (size_t)Ns * ntaps * o.Ci * 2;
-      if (2 * (size_t)pa.second + wbytes > budget) continue;
+      const double a_bytes = (double)s * (BK / 8) * plane;
+      if (plane >> 4 >= (1 << 14)) continue;             // LBO field
       const int ncb = o.Ci / BK;
-      int tg = 0;
-      for (int t = ntaps; t >= 1; --t)
-        if (ntaps % t == 0 && ncb * (ntaps / t) <= 16) { tg = t; break; }
-      if (!tg) continue;
-      const int nab = 2 * (size_t)pa.second + wbytes + pa.second <= budget ? 3 : 2;
-      set_common(ns, BK, tg, ncb * (ntaps / tg), nab, 1);
-      return true;
-    }
-  }
-  // 2. streamed weights: prefer wide K per weight stage (fewer mbarrier round trips)
-  //    while keeping >= 4 stages in flight (weights stream from L2 while the MMAs of
-  //    earlier stages run); fall back to fewer stages only when nothing else fits
-  for (int min_stages = 4; min_stages >= 2; min_stages -= 2)
-    for (int BK = 64; BK >= 16; BK /= 2) {
-      if (o.Ci % BK) continue;
-      const auto pa = a_bytes_of(BK);
-      if (pa.first >> 4 >= (1 << 14)) continue;                       // LBO field
-      const int Ns = p.Np / ns0;
-      const int ncb = o.Ci / BK;
-      for (int tg = ntaps; tg >= 1; --tg) {
-        if (ntaps % tg) continue;
-        const size_t b_bytes = (size_t)tg * Ns * BK * 2;
-        if (2 * (size_t)pa.second + (size_t)min_stages * b_bytes > budget) continue;
-        // up to 4 halo buffers (one per channel block in flight) while >= min_stages weight
-        // stages still fit: with 2 buffers a block's TMA only starts when the MMAs of the block
-        // two back retire, so multi-block layers would wait on TMA latency
-        int nab = 2;
-        while (nab < 4 && nab < ncb && (size_t)(nab + 1) * pa.second + (size_t)min_stages * b_bytes <= budget) ++nab;
-        int stages = (int)((budget - (size_t)nab * pa.second) / b_bytes);
-        if (stages > 16) stages = 16;
-        set_common(ns0, BK, tg, stages, nab, 0);
-        return true;
+      const double m_cb = ntaps * (BK / 16) * t_mma;     // MMAs of one halo block
+      const double t_mmas = ncb * m_cb;
+      for (int resident = 1; resident >= 0; --resident) {
+        if (resident && no_resident) continue;
+        for (int tg = ntaps; tg >= 1; --tg) {
+          if (ntaps % tg) continue;
+          const int nsteps = ncb * (ntaps / tg);
+          const double b_bytes = (double)tg * Ns * BK * 2;
+          if (resident && nsteps > 16) continue;
+          for (int nab = 2; nab <= 4; ++nab) {
+            if (nab > 2 && nab > ncb) break;
+            double wb;
+            int stages;
+            if (resident) {
+              wb = nsteps * b_bytes;
+              stages = nsteps;
+            } else {
+              stages = (int)((budget - nab * a_bytes) / b_bytes);
+              if (stages > 16) stages = 16;
+              if (stages < 2) continue;
+              wb = stages * b_bytes;
+            }
+            if (nab * a_bytes + wb > budget) continue;
+            const double t_halo = ncb * std::max(m_cb, 1.5 / (nab - 1));
+            double t_w = 0.0;
+            if (!resident) {
+              const double copy = 0.55 + b_bytes / 40e3;
+              const double m_step = tg * (BK / 16) * t_mma;
+              t_w = nsteps * std::max(m_step, copy);
+            }
+            const double t_tile = std::max(std::max(t_halo, t_w), t_mmas);
+            const double cost = t_tile + t_epi + (waves - 1) * std::max(t_tile, t_epi);
+            if (cost < best.cost - 1e-9) best = {cost, ns, BK, tg, stages, nab, resident};
+          }
+          if (resident) break;                            // resident: largest tg with <= 16 steps
+        }
       }
     }
-  return false;
+  }
+  if (best.ns == 0) return false;
+  p.nsplit = best.ns;
+  p.Ns = p.Np / best.ns;
+  p.BK = best.BK;
+  p.ncb = o.Ci / best.BK;
+  p.plane = plane;
+  p.phase_bytes = (best.BK / 8) * plane;
+  p.a_bytes = s * p.phase_bytes;
+  p.tg = best.tg;
+  p.b_bytes = best.tg * p.Ns * best.BK * 2;
+  p.stages = best.stages;
+  p.n_abuf = best.nab;
+  p.resident = best.resident;
+  p.n_acc = 2;
+  p.acc_stride = (p.Ns + 31) / 32 * 32;
+  int tc = 32;
+  while (tc < 2 * p.acc_stride) tc *= 2;
+  p.tmem_cols = tc;
+  return true;
 }
 
 static size_t cc_smem(const Op& o) {
@@ -749,6 +751,14 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         }
         const int ncl = std::max(1, std::min(n->S * o.nty * o.ntx, 148 / p.nsplit));
         o.grid_tc = ncl * p.nsplit;
+        static const bool show_plan = getenv("DCNN_TC_PLAN") != nullptr;
+        if (show_plan)
+          fprintf(stderr,
+                  "[dcnn plan] op %d %dx%dx%d->%dx%dx%d k%d s%d: tiles %d nsplit %d Ns %d BK %d ncb %d tg %d steps %d "
+                  "stages %d resident %d halo_bufs %d a_bytes %d b_bytes %d smem %zu grid %d\n",
+                  i, o.Hi, o.Wi, o.Ci, o.H, o.W, o.C, o.kh, o.stride, n->S * o.nty * o.ntx, p.nsplit, p.Ns, p.BK,
+                  p.ncb, p.tg, p.ncb * (o.kh * o.kw / p.tg), p.stages, p.resident, p.n_abuf, p.a_bytes, p.b_bytes,
+                  conv_tc_smem(p), o.grid_tc);
       }
     }
     if (o.kind == DCNN_OP_AFFINE) {
