@@ -65,6 +65,7 @@ struct Op {
   float* wt = nullptr;
   float* bias = nullptr;
   int Cp = 0, K = 0;
+  int ld = 0;                       // channel pitch of delta / O / caches rows (>= C; see create)
   int TH = 8, TW = 8, nty = 0, ntx = 0, STH = 8, STW = 8, WH = 0, WW = 0, CIC = 0, PPT = 1;
   int* list_cc = nullptr;
   int* list_tc = nullptr;
@@ -271,7 +272,7 @@ static size_t cc_smem(const Op& o) {
 static Epi make_epi(dcnn_net* n, int i) {
   Op& o = n->ops[i];
   Epi e;
-  e.C = o.C;
+  e.C = o.ld;                        // row pitch = channels the kernel produces (pad channels stay 0)
   e.act = o.act;
   e.act_param = o.act_param;
   e.eps = n->eps + i + 1;
@@ -642,24 +643,38 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   for (int i = 0; i < L; ++i) n->eps_host[i + 1] = d->layers[i].threshold;
   CUDA_TRY(cudaMemcpy(n->eps, n->eps_host.data(), sizeof(float) * (L + 1), cudaMemcpyHostToDevice));
   int cnt = 0;
+  std::vector<int> n_consumers(L, 0);
+  for (int i = 0; i < L; ++i)
+    for (int j = 0; j < n->ops[i].n_in; ++j)
+      if (n->ops[i].in[j] >= 0) ++n_consumers[n->ops[i].in[j]];
   for (int i = 0; i < L; ++i) {
     Op& o = n->ops[i];
     const dcnn_layer_desc& ld = d->layers[i];
     const size_t px = S * o.H * o.W;
-    if ((r = dalloc(n, &o.delta, px * o.C * es))) return r;
+    // an output-only tensor-core conv whose channel count is not a multiple of 8 (detection /
+    // pose heads: 255, 17) keeps its rows at a pitch rounded up to 8 channels: the pad
+    // channels have zero weights and bias, so they stay exactly 0, and the epilogue runs on
+    // its coalesced 16-byte path; outputs are compacted when they are copied out
+    o.ld = o.C;
+    if (o.kind == DCNN_OP_CONV && o.C % 8 && o.out_slot >= 0 && n_consumers[i] == 0 && o.groups == 1 &&
+        n->dtype == DCNN_F16 && !(n->flags & (DCNN_FLAG_NO_TENSOR_CORES | DCNN_FLAG_HYBRID_DISPATCH)) &&
+        o.Ci % 16 == 0)
+      o.ld = (o.C + 7) / 8 * 8;
+    if ((r = dalloc(n, &o.delta, px * o.ld * es))) return r;
     if ((r = dalloc(n, &o.mask, px))) return r;
     if (o.act != DCNN_ACT_NONE) {
-      if ((r = dalloc(n, &o.xA, px * o.C * n->cesz))) return r;
-      if ((r = dalloc(n, &o.xT, px * o.C * n->cesz))) return r;
+      if ((r = dalloc(n, &o.xA, px * o.ld * n->cesz))) return r;
+      if ((r = dalloc(n, &o.xT, px * o.ld * n->cesz))) return r;
     }
     if (o.kind == DCNN_OP_MAXPOOL && (r = dalloc(n, &o.poolA, S * o.Hi * o.Wi * o.C * n->cesz))) return r;
     if (o.out_slot >= 0) {
-      if ((r = dalloc(n, &o.O, px * o.C * sizeof(float)))) return r;
-      CUDA_TRY(cudaMemset(o.O, 0, px * o.C * sizeof(float)));
+      if ((r = dalloc(n, &o.O, px * o.ld * sizeof(float)))) return r;
+      CUDA_TRY(cudaMemset(o.O, 0, px * o.ld * sizeof(float)));
     }
     if (o.kind == DCNN_OP_CONV) {
       if ((r = plan_cc(o))) return r;
       o.tc = plan_tc(o, n->dtype, n->flags, n->S);
+      if (!o.tc && o.ld != o.C) return fail(DCNN_ERR_UNSUPPORTED, "conv " + std::to_string(i) + ": padded head without tensor-core plan");
       if (o.tc) { o.TH = 16; o.TW = 8; }
       o.K = o.kh * o.kw * (o.Ci_real / o.groups);
       o.nty = (o.H + o.TH - 1) / o.TH;
@@ -687,10 +702,10 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
       }
       if ((r = dalloc(n, &o.wt, wt.size() * 4))) return r;
       CUDA_TRY(cudaMemcpy(o.wt, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice));
-      std::vector<float> b(o.C, 0.f);
+      std::vector<float> b(o.ld, 0.f);                      // pad channels: bias 0
       if (ld.bias) std::copy(ld.bias, ld.bias + o.C, b.begin());
-      if ((r = dalloc(n, &o.bias, o.C * 4))) return r;
-      CUDA_TRY(cudaMemcpy(o.bias, b.data(), o.C * 4, cudaMemcpyHostToDevice));
+      if ((r = dalloc(n, &o.bias, o.ld * 4))) return r;
+      CUDA_TRY(cudaMemcpy(o.bias, b.data(), o.ld * 4, cudaMemcpyHostToDevice));
       const size_t smem = cc_smem(o);
       if (smem > 200 * 1024) return fail(DCNN_ERR_UNSUPPORTED, "conv tile does not fit shared memory");
       if (o.tc) {
@@ -725,7 +740,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         if (o.act != DCNN_ACT_NONE && !n->cache32 && o.C % 8 == 0 && !(n->flags & DCNN_FLAG_HYBRID_DISPATCH)) {
           if ((r = dalloc(n, &p.tflag, S * o.H * o.W))) return r;
           CUDA_TRY(cudaMemset(p.tflag, 0, S * o.H * o.W));
-          CUDA_TRY(cudaMemset(o.xT, 0, S * o.H * o.W * o.C * n->cesz));   // flag 0 <=> x^T == 0
+          CUDA_TRY(cudaMemset(o.xT, 0, S * o.H * o.W * o.ld * n->cesz));   // flag 0 <=> x^T == 0
         }
         // TMA view of the input delta [S][Hi][Wi][Ci] fp16: dims (C, x, y, stream); a box is
         // 8 channels x one stride phase of the halo columns x all halo rows
@@ -850,7 +865,11 @@ dcnn_status dcnn_process_frame(dcnn_net* n, const void* frames, void* const* out
     for (size_t k = 0; k < n->outputs.size(); ++k) {
       const Op& o = n->ops[n->outputs[k]];
       if (!outputs[k]) continue;
-      CUDA_TRY(cudaMemcpyAsync(outputs[k], o.O, (size_t)n->S * o.H * o.W * o.C * 4, cudaMemcpyDeviceToDevice, st));
+      if (o.ld == o.C)
+        CUDA_TRY(cudaMemcpyAsync(outputs[k], o.O, (size_t)n->S * o.H * o.W * o.C * 4, cudaMemcpyDeviceToDevice, st));
+      else   // padded head: compact the rows
+        CUDA_TRY(cudaMemcpy2DAsync(outputs[k], (size_t)o.C * 4, o.O, (size_t)o.ld * 4, (size_t)o.C * 4,
+                                   (size_t)n->S * o.H * o.W, cudaMemcpyDeviceToDevice, st));
     }
   }
   n->last = st;
@@ -870,7 +889,11 @@ dcnn_status dcnn_process_frame_host(dcnn_net* n, const void* host_frames, void* 
     for (size_t k = 0; k < n->outputs.size(); ++k) {
       const Op& o = n->ops[n->outputs[k]];
       if (!host_outputs[k]) continue;
-      CUDA_TRY(cudaMemcpyAsync(host_outputs[k], o.O, (size_t)n->S * o.H * o.W * o.C * 4, cudaMemcpyDeviceToHost, st));
+      if (o.ld == o.C)
+        CUDA_TRY(cudaMemcpyAsync(host_outputs[k], o.O, (size_t)n->S * o.H * o.W * o.C * 4, cudaMemcpyDeviceToHost, st));
+      else
+        CUDA_TRY(cudaMemcpy2DAsync(host_outputs[k], (size_t)o.C * 4, o.O, (size_t)o.ld * 4, (size_t)o.C * 4,
+                                   (size_t)n->S * o.H * o.W, cudaMemcpyDeviceToHost, st));
     }
   }
   n->last = st;
@@ -951,16 +974,26 @@ dcnn_status dcnn_debug_read(dcnn_net* n, int32_t op, int32_t which, void* host, 
   } else {
     const Op& o = n->ops[op];
     const size_t px = (size_t)n->S * o.H * o.W;
+    size_t esz = 0;                    // channel rows at pitch o.ld: compacted to C channels
     switch (which) {
-      case DCNN_BUF_DELTA: src = o.delta; nb = px * o.C * es; break;
+      case DCNN_BUF_DELTA: src = o.delta; esz = es; break;
       case DCNN_BUF_MASK: src = o.mask; nb = px; break;
-      case DCNN_BUF_XA: src = o.xA; nb = px * o.C * n->cesz; break;
-      case DCNN_BUF_XT: src = o.xT; nb = px * o.C * n->cesz; break;
-      case DCNN_BUF_OUT: src = o.O; nb = px * o.C * 4; break;
+      case DCNN_BUF_XA: src = o.xA; esz = n->cesz; break;
+      case DCNN_BUF_XT: src = o.xT; esz = n->cesz; break;
+      case DCNN_BUF_OUT: src = o.O; esz = 4; break;
       case DCNN_BUF_POOLA: src = o.poolA; nb = (size_t)n->S * o.Hi * o.Wi * o.C * n->cesz; break;
       default: return fail(DCNN_ERR_ARG, "which");
     }
     if (!src) return fail(DCNN_ERR_ARG, "buffer not present for this op");
+    if (esz) {
+      nb = px * o.C * esz;
+      if (bytes) *bytes = (int64_t)nb;
+      if (host) {
+        CUDA_TRY(cudaDeviceSynchronize());
+        CUDA_TRY(cudaMemcpy2D(host, o.C * esz, src, o.ld * esz, o.C * esz, px, cudaMemcpyDeviceToHost));
+      }
+      return DCNN_OK;
+    }
   }
   if (bytes) *bytes = (int64_t)nb;
   if (host) {
@@ -1022,7 +1055,7 @@ dcnn_status dcnn_debug_poison(dcnn_net* n) {
   const size_t es = n->esz;
   CUDA_TRY(cudaMemset2D(n->in_delta, n->inCp * es, 0xFF, n->inC * es, (size_t)n->S * n->inH * n->inW));
   for (auto& o : n->ops)
-    CUDA_TRY(cudaMemset(o.delta, 0xFF, (size_t)n->S * o.H * o.W * o.C * es));
+    CUDA_TRY(cudaMemset(o.delta, 0xFF, (size_t)n->S * o.H * o.W * o.ld * es));
   CUDA_TRY(cudaDeviceSynchronize());
   return DCNN_OK;
 }
