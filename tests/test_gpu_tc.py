@@ -122,3 +122,88 @@ def test_deep_nets_fp16_tensor_cores_eps005(make):
     with >= 99.9 % of masks (test_deep_nets_fp32_masks) -- DESIGN.md R-fp16."""
     net, fr = make("f16")
     print("worst", _run(net, fr, tol=5e-2, mask_agree=0.98))
+
+
+def test_tc_per_stream_reset_poison_and_frame_counters():
+    """fp16 tensor-core path, three streams in one launch (the paper's batch): a reset
+    of one stream replays its frame 0 (Z28) while the others continue; NaN-poisoned stale
+    deltas never reach an active output; the device frame counter advances once per
+    frame (end-of-frame bookkeeping folded into the first input-consuming kernel)."""
+    from paper_2203_03996_b200 import DeltaNet, BUF_MASK
+    net = nets.toy_net(64, 64, 64, eps=0.02, dtype="f16")
+    specs = [VideoSpec(64, 64, n_blobs=2, blob_h=10, blob_w=10, speed=3, seed=s) for s in (11, 12, 13)]
+    frames = clip(specs, 9, np.float16)
+    eng = DeltaNet(net, 3)
+    orc = DeltaOracle(net, 3)
+    out = [torch.empty((3,) + s, device="cuda") for s in eng.out_shapes]
+    for t in range(9):
+        if t == 5:
+            eng.reset(1)
+            orc.reset(1)
+        if t > 0:
+            eng.debug_poison()
+        eng.process_frame(torch.from_numpy(frames[t]).cuda(), out)
+        want = orc.step(frames[t])
+        torch.cuda.synchronize()
+        g = out[0].cpu().numpy()
+        assert np.isfinite(g).all()
+        assert max_abs_rel(g, want[0]) <= 2e-2, f"frame {t}"
+        mism, tot = 0, 0
+        for op in range(len(net.layers)):
+            gm = eng.debug_read(op, BUF_MASK).astype(bool)
+            mism += int((gm != orc.masks[op]).sum())
+            tot += gm.size
+        assert 1 - mism / tot >= 0.999, f"frame {t}: mask agreement {1 - mism / tot}"
+    assert eng.stats()["frame_index"] == 9
+    eng.close()
+
+
+def test_tc_static_clip_skips_every_tile():
+    """fp16 tensor-core path: a repeated frame gives all-empty masks at every layer, every
+    tile skipped by the fused scout, and a bit-identical output (Z1)."""
+    from paper_2203_03996_b200 import DeltaNet, BUF_MASK
+    net = nets.toy_net(64, 64, 64, eps=0.0, dtype="f16")
+    fr = clip([VideoSpec(64, 64, n_blobs=2, blob_h=8, blob_w=8, seed=3)], 1, np.float16)[0]
+    eng = DeltaNet(net, 1)
+    out = [torch.empty((1,) + s, device="cuda") for s in eng.out_shapes]
+    x = torch.from_numpy(fr).cuda()
+    eng.process_frame(x, out)
+    first = out[0].clone()
+    for _ in range(3):
+        eng.process_frame(x, out)
+        torch.cuda.synchronize()
+        assert torch.equal(out[0], first)
+        for op in range(-1, len(net.layers)):
+            assert eng.debug_read(op, BUF_MASK).sum() == 0
+    st = eng.stats()
+    for i, L in enumerate(net.layers):
+        if L.op == "conv":
+            r = st["ops"][i + 1]
+            assert r["tiles_skip"] == r["tiles_total"] > 0
+    eng.close()
+
+
+@pytest.mark.parametrize("co", [255, 17])
+def test_tc_padded_head_rows(co):
+    """Output-only heads with C_out % 8 != 0 run with 8-channel-aligned internal rows; the
+    outputs and debug reads are compacted back to C_out channels."""
+    from paper_2203_03996_b200 import BUF_OUT, BUF_DELTA
+    b = nets._Builder("head", 24, 20, 64, 7, "f16")
+    i = b.conv(-1, co, 1)
+    b.net.outputs = [i]
+    b.net.input_eps = 0.0
+    net = b.net
+    frames = _frames(net, 5, 4)
+    from paper_2203_03996_b200 import DeltaNet
+    eng = DeltaNet(net, 1)
+    orc = DeltaOracle(net, 1)
+    out = [torch.empty((1,) + s, device="cuda") for s in eng.out_shapes]
+    for t in range(frames.shape[0]):
+        eng.process_frame(torch.from_numpy(frames[t]).cuda(), out)
+        want = orc.step(frames[t])
+        torch.cuda.synchronize()
+        assert out[0].shape[-1] == co
+        assert max_abs_rel(out[0].cpu().numpy(), want[0]) <= 2e-2
+        np.testing.assert_array_equal(eng.debug_read(i, BUF_OUT).reshape(out[0].shape), out[0].cpu().numpy())
+        assert eng.debug_read(i, BUF_DELTA).size == 24 * 20 * co
+    eng.close()
