@@ -431,14 +431,16 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       pp.G = group_lanes(o.C);
       pp.ep = make_epi(n, i);
       const bool lean_pool = lean_pool_ok(pp, n->dtype);
+      const bool win_pool = !lean_pool && lean_pool_win_ok(pp, n->dtype);
       {
         TimeScope ts(n, ost, DCNN_KCLASS_POINTWISE, i);
         if (lean_pool) launch_maxpool_disj(pp, n->cache32, ost);       // pool + A update, one launch
+        else if (win_pool) launch_maxpool_win(pp, n->cache32, ost);     // pool, then A update
         else if (lean_up_ok(pp, n->dtype)) launch_up_lean(pp, ost);
         else launch_pointwise(pp, n->dtype, n->cache32, ost);
       }
-      ++k;
-      if (o.kind == DCNN_OP_MAXPOOL && !lean_pool) {
+      k += win_pool ? 2 : 1;
+      if (o.kind == DCNN_OP_MAXPOOL && !lean_pool && !win_pool) {
         TimeScope ts(n, ost, DCNN_KCLASS_POINTWISE, i);
         launch_pool_update(pp, n->dtype, n->cache32, ost);
         ++k;

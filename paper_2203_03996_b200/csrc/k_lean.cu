@@ -158,6 +158,120 @@ __global__ void __launch_bounds__(256) k_maxpool_disj(PwParams p, int lg_nch) {
   warp_count_flush(p.ep.n_active, lane, n);
 }
 
+// ---------------------------------------------------------------- a7, overlapping windows
+// k x k max-pool, any stride and padding (YOLOv5s SPPF: 5x5 s1 p2): Eq. 3 on the
+// accumulated input A (the A update is a separate pass, windows overlap).  Thread = (output
+// pixel, 8-channel chunk); the loads of one window row (masks, deltas, accumulated values)
+// are issued together, so a window costs k round trips instead of k*k.
+template <typename T, typename TC, int KK>
+__global__ void __launch_bounds__(256) k_maxpool_win(PwParams p, int lg_nch) {
+  pdl_trigger();
+  pdl_wait();
+  frame_bookkeeping(p.ep);
+  const int C = p.ep.C, nch = 1 << lg_nch;
+  const long long nout = (long long)p.S * p.H * p.W;
+  const long long HWo = (long long)p.H * p.W;
+  const T* din = reinterpret_cast<const T*>(p.in[0]);
+  T* dout = reinterpret_cast<T*>(p.ep.delta);
+  const TC* A = reinterpret_cast<const TC*>(p.poolA);
+  unsigned nact = 0;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < (nout << lg_nch);
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long q = g >> lg_nch;
+    const int j = (int)(g & (nch - 1));
+    const int s = (int)(q / HWo);
+    const int rem = (int)(q - (long long)s * HWo);
+    const int y = rem / p.W, x = rem - (rem / p.W) * p.W;
+    const long long sbase = (long long)s * p.Hi * p.Wi;
+    const bool first = p.ep.first[s] != 0;
+    float mnew[8], mold[8];
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) mnew[c] = mold[c] = -INFINITY;
+    for (int ky = 0; ky < KK; ++ky) {
+      const int iy = y * p.stride - p.pad + ky;
+      if (iy < 0 || iy >= p.Hi) continue;               // padding: -inf, never active
+      uint8_t mk[KK];
+      float d[KK][8], a[KK][8];
+#pragma unroll
+      for (int kx = 0; kx < KK; ++kx) {                   // the row's loads, all in flight
+        const int ix = x * p.stride - p.pad + kx;
+        mk[kx] = 0;
+        if (ix >= 0 && ix < p.Wi) {
+          const long long ip = sbase + (long long)iy * p.Wi + ix;
+          mk[kx] = first ? 1 : p.min[0][ip];
+          ld8(din + ip * C + 8 * j, d[kx]);
+          if (!first) ld8(A + ip * C + 8 * j, a[kx]);
+        }
+      }
+#pragma unroll
+      for (int kx = 0; kx < KK; ++kx) {
+        const int ix = x * p.stride - p.pad + kx;
+        if (ix < 0 || ix >= p.Wi) continue;
+        const bool on = mk[kx] != 0;
+        any |= on;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float av = first ? 0.f : a[kx][c];
+          mnew[c] = fmaxf(mnew[c], av + (on ? d[kx][c] : 0.f));   // select: stale deltas unused
+          mold[c] = fmaxf(mold[c], av);
+        }
+      }
+    }
+    if (j == 0) p.ep.mask[q] = any ? 1 : 0;
+    if (any) {
+      float o[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) o[c] = rnd<T>(first ? mnew[c] : mnew[c] - mold[c]);   // Eq. 3
+      st8(dout + q * C + 8 * j, o);
+      if (p.ep.O) {
+        float* O = p.ep.O + q * C + 8 * j;
+        float ov[8];
+        if (first) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) ov[c] = 0.f;
+        } else {
+          ld8(O, ov);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) ov[c] += o[c];
+        st8(O, ov);
+      }
+      if (j == 0) ++nact;
+    }
+  }
+  const int lane = threadIdx.x & 31;
+  unsigned n = (unsigned)warp_sum((int)nact);
+  warp_count_flush(p.ep.n_active, lane, n);
+}
+
+// A := A + dx~ on the active input pixels, 16 bytes per thread (after the pool read old A)
+template <typename T, typename TC>
+__global__ void __launch_bounds__(256) k_pool_update_vec(PwParams p, int lg_nch) {
+  pdl_trigger();
+  pdl_wait();
+  const int C = p.ep.C, nch = 1 << lg_nch;
+  const long long HWi = (long long)p.Hi * p.Wi;
+  const long long npx = (long long)p.S * HWi;
+  const T* d = reinterpret_cast<const T*>(p.in[0]);
+  TC* A = reinterpret_cast<TC*>(p.poolA);
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < (npx << lg_nch);
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long q = g >> lg_nch;
+    const int j = (int)(g & (nch - 1));
+    const bool first = p.ep.first[q / HWi] != 0;
+    const uint8_t m = p.min[0][q];
+    float dv[8], av[8];
+    ld8(d + q * C + 8 * j, dv);
+    if (!first) ld8(A + q * C + 8 * j, av);
+    if (first || m) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) av[c] = (first ? 0.f : av[c]) + dv[c];
+      st8(A + q * C + 8 * j, av);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- a6, nearest upsample
 template <typename T>
 __global__ void __launch_bounds__(256) k_up_lean(PwParams p, int lg_nch) {
@@ -206,6 +320,26 @@ static int log2_exact(int v) {
 bool lean_pool_ok(const PwParams& p, int dtype) {
   return dtype == 1 && p.kind == 2 && p.k == 2 && p.stride == 2 && p.pad == 0 && p.Hi % p.k == 0 &&
          p.Wi % p.k == 0 && p.ep.C % 8 == 0 && log2_exact(p.ep.C / 8) >= 0 && p.ep.act == 0;
+}
+
+bool lean_pool_win_ok(const PwParams& p, int dtype) {
+  return dtype == 1 && p.kind == 2 && (p.k == 5 || p.k == 3) && p.ep.C % 8 == 0 && log2_exact(p.ep.C / 8) >= 0 &&
+         p.ep.act == 0;
+}
+
+void launch_maxpool_win(const PwParams& p, int cache32, cudaStream_t st) {
+  const int lg = log2_exact(p.ep.C / 8);
+  const int grid = lean_grid(((long long)p.S * p.H * p.W) << lg);
+  const int gridu = lean_grid(((long long)p.S * p.Hi * p.Wi) << lg);
+  if (p.k == 5) {
+    if (cache32) launch_k(k_maxpool_win<__half, float, 5>, dim3(grid), dim3(256), 0, st, 1, p, lg);
+    else launch_k(k_maxpool_win<__half, __half, 5>, dim3(grid), dim3(256), 0, st, 1, p, lg);
+  } else {
+    if (cache32) launch_k(k_maxpool_win<__half, float, 3>, dim3(grid), dim3(256), 0, st, 1, p, lg);
+    else launch_k(k_maxpool_win<__half, __half, 3>, dim3(grid), dim3(256), 0, st, 1, p, lg);
+  }
+  if (cache32) launch_k(k_pool_update_vec<__half, float>, dim3(gridu), dim3(256), 0, st, 1, p, lg);
+  else launch_k(k_pool_update_vec<__half, __half>, dim3(gridu), dim3(256), 0, st, 1, p, lg);
 }
 
 bool lean_up_ok(const PwParams& p, int dtype) {

@@ -123,6 +123,8 @@ void launch_pool_update(const PwParams& p, int dtype, int cache32, cudaStream_t 
 void launch_input_r0(const InputParams& p, int dtype, cudaStream_t st);   // radius 0, C <= 4
 bool lean_pool_ok(const PwParams& p, int dtype);       // 2x2 s2 max-pool, fp16, C/8 power of 2
 void launch_maxpool_disj(const PwParams& p, int cache32, cudaStream_t st);   // pool + A update
+bool lean_pool_win_ok(const PwParams& p, int dtype);   // 3x3 / 5x5 max-pool (overlapping windows), fp16
+void launch_maxpool_win(const PwParams& p, int cache32, cudaStream_t st);    // pool, then A update
 bool lean_up_ok(const PwParams& p, int dtype);         // nearest upsample, fp16, C/8 power of 2
 void launch_up_lean(const PwParams& p, cudaStream_t st);
 
