@@ -201,6 +201,7 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
     const double t_epi = 3.5 + 0.35 * std::max(0, c_thread - 32) + (ns > 1 ? 1.0 : 0.0);
     for (int BK = 64; BK >= 16; BK /= 2) {
       if (o.Ci % BK) continue;
+      if (o.kh == 1 && o.kw == 1 && s == 1 && o.Ci % 64 == 0 && BK != 64) continue;   // swizzled path
       const double a_bytes = (double)s * (BK / 8) * plane;
       if (plane >> 4 >= (1 << 14)) continue;             // LBO field
       const int ncb = o.Ci / BK;
@@ -244,6 +245,8 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
     }
   }
   if (best.ns == 0) return false;
+  static const bool no_sw = getenv("DCNN_TC_NO_SW128") != nullptr;
+  p.sw128 = (!no_sw && o.kh == 1 && o.kw == 1 && s == 1 && best.BK == 64) ? 1 : 0;
   p.nsplit = best.ns;
   p.Ns = p.Np / best.ns;
   p.BK = best.BK;
@@ -759,10 +762,11 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
           const cuuint64_t gdim[4] = {(cuuint64_t)o.Ci, (cuuint64_t)o.Wi, (cuuint64_t)o.Hi, (cuuint64_t)n->S};
           const cuuint64_t gstr[3] = {(cuuint64_t)o.Ci * 2, (cuuint64_t)o.Wi * o.Ci * 2,
                                       (cuuint64_t)o.Hi * o.Wi * o.Ci * 2};
-          const cuuint32_t box[4] = {8, (cuuint32_t)(o.stride * p.WQ), (cuuint32_t)p.HH, 1};
+          const cuuint32_t box[4] = {p.sw128 ? 64u : 8u, (cuuint32_t)(o.stride * p.WQ), (cuuint32_t)p.HH, 1};
           const cuuint32_t es[4] = {1, (cuuint32_t)o.stride, 1, 1};
           CUresult cr = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, src, gdim, gstr, box, es,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               p.sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
           if (cr != CUDA_SUCCESS) return fail(DCNN_ERR_CUDA, "conv " + std::to_string(i) + ": tensor map encode failed");
         }
@@ -772,10 +776,10 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         if (show_plan)
           fprintf(stderr,
                   "[dcnn plan] op %d %dx%dx%d->%dx%dx%d k%d s%d: tiles %d nsplit %d Ns %d BK %d ncb %d tg %d steps %d "
-                  "stages %d resident %d halo_bufs %d a_bytes %d b_bytes %d smem %zu grid %d\n",
+                  "stages %d resident %d halo_bufs %d a_bytes %d b_bytes %d smem %zu grid %d sw128 %d\n",
                   i, o.Hi, o.Wi, o.Ci, o.H, o.W, o.C, o.kh, o.stride, n->S * o.nty * o.ntx, p.nsplit, p.Ns, p.BK,
                   p.ncb, p.tg, p.ncb * (o.kh * o.kw / p.tg), p.stages, p.resident, p.n_abuf, p.a_bytes, p.b_bytes,
-                  conv_tc_smem(p), o.grid_tc);
+                  conv_tc_smem(p), o.grid_tc, p.sw128);
       }
     }
     if (o.kind == DCNN_OP_AFFINE) {

@@ -360,9 +360,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       for (int px = (p.dbg & 8) ? npx : lt; px < npx; px += 32) {   // dbg 8: no zero pass (timing only)
         const int iy = pg_iy0 + hy, ix = pg_ix0 + hx;
         if (!hm[px] && iy >= 0 && iy < p.H && ix >= 0 && ix < p.W) {
-          unsigned char* d = A + (hx & lgs) * p.phase_bytes + (hy * p.WQ + (hx >> lgs)) * 16;
-          for (int ch = 0; ch < nch; ++ch)
-            *reinterpret_cast<uint4*>(d + ch * p.plane) = make_uint4(0u, 0u, 0u, 0u);
+          if (p.sw128) {                       // the pixel's whole 128-B row (swizzle permutes within it)
+            unsigned char* d = A + px * 128;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) *reinterpret_cast<uint4*>(d + ch * 16) = make_uint4(0u, 0u, 0u, 0u);
+          } else {
+            unsigned char* d = A + (hx & lgs) * p.phase_bytes + (hy * p.WQ + (hx >> lgs)) * 16;
+            for (int ch = 0; ch < nch; ++ch)
+              *reinterpret_cast<uint4*>(d + ch * p.plane) = make_uint4(0u, 0u, 0u, 0u);
+          }
         }
         hx += dx32;
         hy += dy32;
@@ -381,6 +387,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         if (p.dbg & 16) { tc::mbar_arrive(&a_tma[b]); return; }   // dbg 16: no halo copies (timing only)
         tc::mbar_arrive_expect_tx(&a_tma[b], gbytes);
         const uint32_t A = tc::smem_u32(smem + L.a0 + b * p.a_bytes);
+        if (p.sw128) {                         // one box: 64 channels x 8 columns x 16 rows, swizzled
+          tma_load_4d(A, &p.tmap, cb * p.BK, ix0, iy0, s, &a_tma[b]);
+          return;
+        }
         // one box of 8 channels x (columns of one stride phase) x halo rows per plane
         for (int ph = 0; ph < p.stride; ++ph)
           for (int ch = 0; ch < nch; ++ch)
@@ -495,12 +505,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             // all MMAs of tg taps x BK/16 K-steps against one weight step
             uint32_t accum = (cb | g) != 0;
             for (int t = 0; t < p.tg; ++t) {
-              uint64_t ad = tc::smem_desc(abase + tapoff[g * p.tg + t], p.plane, sbo_a);
+              uint64_t ad = p.sw128 ? tc::smem_desc_sw128(abase, 1024)
+                                    : tc::smem_desc(abase + tapoff[g * p.tg + t], p.plane, sbo_a);
+              const uint64_t a_inc = p.sw128 ? 2 : a_step;   // K = 16: +32 B inside the swizzled row
               uint64_t bd = tc::smem_desc(bbase + (uint32_t)(t * p.Ns * p.BK * 2), lbo_b, 128);
               for (int kc = 0; kc < nk; ++kc) {
                 tc::mma_f16(dbase, ad, bd, idesc, accum);
                 accum = 1;
-                ad += a_step;                    // start address: + 2 planes (A) per K = 16
+                ad += a_inc;                     // start address: + 2 planes (A) per K = 16
                 bd += b_step;                    // + 2 core-matrix chunks (B)
               }
             }

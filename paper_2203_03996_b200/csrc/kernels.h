@@ -80,6 +80,8 @@ struct ConvTCParams {
   int n_abuf;                   // halo buffers (2..4)
   int resident;                 // 1: all weight steps of the CTA stay in smem (stages = steps)
   int tg;                       // taps per weight stage (divides kh*kw)
+  int sw128;                    // 1x1 s1 convs, BK = 64: halo rows of 128 B (one pixel's channel
+                                // block) in the 128-byte-swizzled K-major layout, one TMA box per block
   int n_acc, acc_stride;        // TMEM accumulators and their column stride
   int tmem_cols;
   int nsplit, Ns;               // output channels split over a cluster of nsplit CTAs (Ns each)

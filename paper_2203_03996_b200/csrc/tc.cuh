@@ -181,6 +181,19 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
+// K-major, 128-byte swizzle (canonical Swizzle<3,4,3> o ((8,m),2):((8,SBO),1) in 16-byte units):
+// 8 rows of 128 B form an atom, SBO = byte distance of consecutive 8-row groups, LBO = 1
+// (unused), layout type 2 at bits [61,64).  The K = 16 slice k of a row is at +32 B * k.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 // Instruction descriptor kind::f16: A,B fp16 (format 0), D fp32 (c_format=1 at bit 4),
 // both K-major, N>>3 at bit 17, M>>4 at bit 24.
 __host__ __device__ __forceinline__ uint32_t idesc_f16(int M, int N) {
