@@ -98,14 +98,18 @@ struct dcnn_net {
   int bookkeeper = -1;              // op whose kernel clears pend and advances frame_idx
   long long* frame_idx = nullptr;
   int* err = nullptr;
-  int* err_host = nullptr;          // pinned mirror, refreshed at the end of every frame
+  int* err_host = nullptr;          // mapped pinned sticky error word (n->err is its device alias)
   float* eps = nullptr;             // [n_ops + 1], slot 0 = input
   unsigned long long* stats = nullptr;  // [(n_ops + 1) * 8]
   int* counts = nullptr;            // [2 * n_convs]
   int n_counts = 0;
   std::vector<float> eps_host;
   std::vector<void*> allocs;
-  // graph
+  // graph; the input-kernel and output-copy nodes get per-call parameters (caller's frame and
+  // output pointers), so no copy sits outside the graph
+  cudaGraphNode_t node_input = nullptr, node_out = nullptr;
+  InputParams ip_cap;
+  OutCopyParams oc_cap;
   cudaStream_t cap = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -329,6 +333,16 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
     else launch_input(ip, n->dtype, st);
   }
   ++k;
+  {
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    if (cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &nd) == cudaSuccess &&
+        cs == cudaStreamCaptureStatusActive && nd == 1 && n->timing_mask == 0) {
+      n->node_input = deps[0];
+      n->ip_cap = ip;
+    }
+  }
   if (!n->aux.empty()) cudaEventRecord(n->ev_input, st);
   auto src_delta = [&](int j) -> const void* { return j < 0 ? n->in_delta : n->ops[j].delta; };
   auto src_mask = [&](int j) -> const uint8_t* { return j < 0 ? n->in_mask : n->ops[j].mask; };
@@ -455,8 +469,52 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
     cudaEventRecord(n->ev_join[k2 - 1], n->aux[k2 - 1]);
     cudaStreamWaitEvent(st, n->ev_join[k2 - 1], 0);
   }
-  cudaMemcpyAsync(n->err_host, n->err, sizeof(int), cudaMemcpyDeviceToHost, st);
+  // dense outputs to the caller's buffers (destinations set per call; none while capturing)
+  OutCopyParams oc;
+  memset(&oc, 0, sizeof(oc));
+  oc.n = (int)n->outputs.size();
+  for (int q = 0; q < oc.n; ++q) {
+    const Op& o = n->ops[n->outputs[q]];
+    oc.src[q] = o.O;
+    oc.rows[q] = (long long)n->S * o.H * o.W;
+    oc.C[q] = o.C;
+    oc.ld[q] = o.ld;
+  }
+  launch_copy_out(oc, st);
+  ++k;
+  {
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    if (cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &nd) == cudaSuccess &&
+        cs == cudaStreamCaptureStatusActive && nd == 1) {
+      n->node_out = deps[0];
+      n->oc_cap = oc;
+    }
+  }
   if (kcount) *kcount = k;
+}
+
+// per-call parameters of the input-kernel and output-copy nodes of the instantiated graph
+static dcnn_status set_frame_io(dcnn_net* n, const void* frame, void* const* outputs) {
+  if (!n->node_input || !n->node_out) return fail(DCNN_ERR_CUDA, "frame graph nodes not found");
+  cudaKernelNodeParams kp;
+  CUDA_TRY(cudaGraphKernelNodeGetParams(n->node_input, &kp));
+  InputParams ip = n->ip_cap;
+  ip.frame = frame;
+  void* a_in[] = {&ip};
+  kp.kernelParams = a_in;
+  kp.extra = nullptr;
+  CUDA_TRY(cudaGraphExecKernelNodeSetParams(n->exec, n->node_input, &kp));
+  cudaKernelNodeParams ko;
+  CUDA_TRY(cudaGraphKernelNodeGetParams(n->node_out, &ko));
+  OutCopyParams oc = n->oc_cap;
+  for (int q = 0; q < oc.n; ++q) oc.dst[q] = outputs ? reinterpret_cast<float*>(outputs[q]) : nullptr;
+  void* a_out[] = {&oc};
+  ko.kernelParams = a_out;
+  ko.extra = nullptr;
+  CUDA_TRY(cudaGraphExecKernelNodeSetParams(n->exec, n->node_out, &ko));
+  return DCNN_OK;
 }
 
 static dcnn_status build_graph(dcnn_net* n) {
@@ -606,6 +664,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
     o.Ci_real = o.Ci;
     if (o.in[0] < 0) o.Ci = n->inCp;
   }
+  if (d->n_outputs > MAX_OUT) return fail(DCNN_ERR_UNSUPPORTED, "at most 8 output ops");
   for (int k = 0; k < d->n_outputs; ++k) {
     int j = d->output_ops[k];
     if (j < 0 || j >= L) return fail(DCNN_ERR_ARG, "output op index");
@@ -626,7 +685,11 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   if ((r = dalloc(n, &n->first, S))) return r;
   if ((r = dalloc(n, &n->pend, S))) return r;
   if ((r = dalloc(n, &n->frame_idx, S * sizeof(long long)))) return r;
-  if ((r = dalloc(n, &n->err, sizeof(int)))) return r;
+  // sticky error word in mapped pinned memory: the (rare) device write lands in host memory,
+  // so no per-frame copy node is needed to check it
+  CUDA_TRY(cudaHostAlloc(&n->err_host, sizeof(int), cudaHostAllocMapped));
+  *n->err_host = 0;
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&n->err), n->err_host, 0));
   if ((r = dalloc(n, &n->eps, sizeof(float) * (L + 1)))) return r;
   if ((r = dalloc(n, &n->stats, sizeof(unsigned long long) * 8 * (L + 1)))) return r;
   n->n_counts = 2 * n_convs;
@@ -639,10 +702,9 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
     for (int j = 0; j < n->ops[i].n_in; ++j)
       if (n->ops[i].in[j] < 0) n->bookkeeper = i;
   CUDA_TRY(cudaMemset(n->frame_idx, 0, S * sizeof(long long)));
-  CUDA_TRY(cudaMemset(n->err, 0, sizeof(int)));
+
   CUDA_TRY(cudaMemset(n->P, 0, n->frame_bytes));
-  CUDA_TRY(cudaHostAlloc(&n->err_host, sizeof(int), cudaHostAllocDefault));
-  *n->err_host = 0;
+
   n->eps_host.assign(L + 1, 0.f);
   n->eps_host[0] = d->input_threshold;
   for (int i = 0; i < L; ++i) n->eps_host[i + 1] = d->layers[i].threshold;
@@ -854,7 +916,7 @@ dcnn_status dcnn_reset(dcnn_net* n, int32_t stream) {
 }
 
 static dcnn_status check_err(dcnn_net* n) {
-  if (*n->err_host) return fail(DCNN_ERR_NONFINITE, "non-finite value in an input frame (sticky)");
+  if (*(volatile int*)n->err_host) return fail(DCNN_ERR_NONFINITE, "non-finite value in an input frame (sticky)");
   return DCNN_OK;
 }
 
@@ -865,18 +927,21 @@ dcnn_status dcnn_process_frame(dcnn_net* n, const void* frames, void* const* out
   if (s) return s;
   if ((s = build_graph(n))) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  CUDA_TRY(cudaMemcpyAsync(n->frame_in, frames, n->frame_bytes, cudaMemcpyDeviceToDevice, st));
-  CUDA_TRY(cudaGraphLaunch(n->exec, st));
-  if (outputs) {
-    for (size_t k = 0; k < n->outputs.size(); ++k) {
-      const Op& o = n->ops[n->outputs[k]];
-      if (!outputs[k]) continue;
-      if (o.ld == o.C)
-        CUDA_TRY(cudaMemcpyAsync(outputs[k], o.O, (size_t)n->S * o.H * o.W * o.C * 4, cudaMemcpyDeviceToDevice, st));
-      else   // padded head: compact the rows
-        CUDA_TRY(cudaMemcpy2DAsync(outputs[k], (size_t)o.C * 4, o.O, (size_t)o.ld * 4, (size_t)o.C * 4,
-                                   (size_t)n->S * o.H * o.W, cudaMemcpyDeviceToDevice, st));
-    }
+  if (n->timing_mask) {
+    // profiling graph (no per-call nodes): stage the frame and copy outputs around it
+    CUDA_TRY(cudaMemcpyAsync(n->frame_in, frames, n->frame_bytes, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaGraphLaunch(n->exec, st));
+    if (outputs)
+      for (size_t k = 0; k < n->outputs.size(); ++k) {
+        const Op& o = n->ops[n->outputs[k]];
+        if (outputs[k])
+          CUDA_TRY(cudaMemcpy2DAsync(outputs[k], (size_t)o.C * 4, o.O, (size_t)o.ld * 4, (size_t)o.C * 4,
+                                     (size_t)n->S * o.H * o.W, cudaMemcpyDeviceToDevice, st));
+      }
+  } else {
+    // the input kernel reads the caller's frame, the graph's last kernel writes the outputs
+    if ((s = set_frame_io(n, frames, outputs))) return s;
+    CUDA_TRY(cudaGraphLaunch(n->exec, st));
   }
   n->last = st;
   return DCNN_OK;
@@ -890,6 +955,7 @@ dcnn_status dcnn_process_frame_host(dcnn_net* n, const void* host_frames, void* 
   if ((s = build_graph(n))) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaMemcpyAsync(n->frame_in, host_frames, n->frame_bytes, cudaMemcpyHostToDevice, st));
+  if (!n->timing_mask && (s = set_frame_io(n, n->frame_in, nullptr))) return s;
   CUDA_TRY(cudaGraphLaunch(n->exec, st));
   if (host_outputs) {
     for (size_t k = 0; k < n->outputs.size(); ++k) {
@@ -924,8 +990,7 @@ dcnn_status dcnn_get_stats(dcnn_net* n, dcnn_op_stats* per_op, int64_t* frame_in
   CUDA_TRY(cudaMemcpy(raw.data(), n->stats, raw.size() * 8, cudaMemcpyDeviceToHost));
   long long fi = 0;
   CUDA_TRY(cudaMemcpy(&fi, n->frame_idx, sizeof(long long), cudaMemcpyDeviceToHost));
-  int err = 0;
-  CUDA_TRY(cudaMemcpy(&err, n->err, sizeof(int), cudaMemcpyDeviceToHost));
+  const int err = *(volatile int*)n->err_host;
   if (frame_index) *frame_index = fi;
   if (device_error) *device_error = err ? DCNN_ERR_NONFINITE : DCNN_OK;
   if (per_op) {

@@ -306,6 +306,34 @@ __global__ void __launch_bounds__(256) k_up_lean(PwParams p, int lg_nch) {
   warp_count_flush(p.ep.n_active, lane, n);
 }
 
+// ---------------------------------------------------------------- outputs to the caller
+__global__ void __launch_bounds__(256) k_copy_out(OutCopyParams p) {
+  pdl_trigger();
+  pdl_wait();
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  for (int k = 0; k < p.n; ++k) {
+    float* dst = p.dst[k];
+    if (!dst) continue;
+    const float* src = p.src[k];
+    const long long n = p.rows[k] * p.C[k];
+    if (p.C[k] == p.ld[k] && n % 4 == 0 && ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      float4* d4 = reinterpret_cast<float4*>(dst);
+      for (long long i = tid; i < n / 4; i += nth) d4[i] = s4[i];
+    } else {                                   // padded head rows (ld > C) or unaligned buffers
+      for (long long i = tid; i < n; i += nth) {
+        const long long r = i / p.C[k];
+        dst[i] = src[r * p.ld[k] + (i - r * p.C[k])];
+      }
+    }
+  }
+}
+
+void launch_copy_out(const OutCopyParams& p, cudaStream_t st) {
+  launch_k(k_copy_out, dim3(148 * 4), dim3(256), 0, st, 1, p);
+}
+
 static int lean_grid(long long items) {
   long long blocks = (items + 255) / 256;
   return (int)(blocks < 1 ? 1 : (blocks < 148 * 16 ? blocks : 148 * 16));

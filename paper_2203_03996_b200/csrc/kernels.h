@@ -130,6 +130,19 @@ void launch_maxpool_win(const PwParams& p, int cache32, cudaStream_t st);    // 
 bool lean_up_ok(const PwParams& p, int dtype);         // nearest upsample, fp16, C/8 power of 2
 void launch_up_lean(const PwParams& p, cudaStream_t st);
 
+// ---------------------------------------------------------------- outputs
+// Copy of the dense outputs O (fp32, rows at pitch ld) into the caller's buffers (rows of C),
+// the last node of the frame graph (PDL-chained, destinations updated per call)
+constexpr int MAX_OUT = 8;
+struct OutCopyParams {
+  int n;
+  const float* src[MAX_OUT];
+  float* dst[MAX_OUT];          // null: not requested this frame
+  long long rows[MAX_OUT];      // S * H * W
+  int C[MAX_OUT], ld[MAX_OUT];
+};
+void launch_copy_out(const OutCopyParams& p, cudaStream_t st);
+
 // ---------------------------------------------------------------- control
 
 }  // namespace dcnn
