@@ -341,6 +341,26 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Input kernels: reset the per-frame counters of the later ops (block 0) and publish this
+// CTA's active-pixel count (one plain store per CTA, no pre-zeroed accumulator needed).
+__device__ __forceinline__ void input_frame_counters(unsigned long long* zero_stats, int n_zero_stats,
+                                                     int* zero_counts, int n_zero_counts,
+                                                     unsigned long long* cta_active, unsigned nact) {
+  __shared__ unsigned block_cnt;
+  if (threadIdx.x == 0) block_cnt = 0;
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < n_zero_stats; i += blockDim.x) zero_stats[i] = 0ull;
+    for (int i = threadIdx.x; i < n_zero_counts; i += blockDim.x) zero_counts[i] = 0;
+  }
+  __syncthreads();
+  unsigned w = nact;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+  if ((threadIdx.x & 31) == 0 && w) atomicAdd(&block_cnt, w);
+  __syncthreads();
+  if (threadIdx.x == 0) cta_active[blockIdx.x] = block_cnt;
+}
+
 // Flush a per-warp counter with one atomic (lane 0 holds the count).
 __device__ __forceinline__ void warp_count_flush(unsigned long long* ctr, int lane, unsigned n) {
   if (ctr && lane == 0 && n) atomicAdd(ctr, (unsigned long long)n);

@@ -100,7 +100,8 @@ struct dcnn_net {
   int* err = nullptr;
   int* err_host = nullptr;          // mapped pinned sticky error word (n->err is its device alias)
   float* eps = nullptr;             // [n_ops + 1], slot 0 = input
-  unsigned long long* stats = nullptr;  // [(n_ops + 1) * 8]
+  unsigned long long* stats = nullptr;  // [(n_ops + 1) * 8]; slot 0's active count lives in cta_active
+  unsigned long long* cta_active = nullptr;  // [INPUT_MAX_GRID] active input pixels per input-kernel CTA
   int* counts = nullptr;            // [2 * n_convs]
   int n_counts = 0;
   std::vector<float> eps_host;
@@ -321,12 +322,13 @@ struct TimeScope {
 static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
   int k = 0;
   const int nops = (int)n->ops.size();
-  cudaMemsetAsync(n->stats, 0, sizeof(unsigned long long) * 8 * (nops + 1), st);
-  if (n->n_counts) cudaMemsetAsync(n->counts, 0, sizeof(int) * n->n_counts, st);
   InputParams ip;
   ip.S = n->S; ip.H = n->inH; ip.W = n->inW; ip.C = n->inC; ip.Cp = n->inCp; ip.radius = n->radius;
   ip.frame = n->frame_in; ip.P = n->P; ip.delta = n->in_delta; ip.mask = n->in_mask;
-  ip.eps = n->eps; ip.first = n->first; ip.pend = n->pend; ip.err = n->err; ip.n_active = n->stats + 1;
+  ip.eps = n->eps; ip.first = n->first; ip.pend = n->pend; ip.err = n->err;
+  ip.cta_active = n->cta_active;
+  ip.zero_stats = n->stats + 8; ip.n_zero_stats = 8 * nops;   // slot 0 (the input) is per-CTA
+  ip.zero_counts = n->counts; ip.n_zero_counts = n->n_counts;
   {
     TimeScope ts(n, st, DCNN_KCLASS_INPUT);
     if (ip.radius == 0 && ip.C <= 4) launch_input_r0(ip, n->dtype, st);
@@ -692,6 +694,9 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&n->err), n->err_host, 0));
   if ((r = dalloc(n, &n->eps, sizeof(float) * (L + 1)))) return r;
   if ((r = dalloc(n, &n->stats, sizeof(unsigned long long) * 8 * (L + 1)))) return r;
+  CUDA_TRY(cudaMemset(n->stats, 0, sizeof(unsigned long long) * 8 * (L + 1)));
+  if ((r = dalloc(n, &n->cta_active, sizeof(unsigned long long) * INPUT_MAX_GRID))) return r;
+  CUDA_TRY(cudaMemset(n->cta_active, 0, sizeof(unsigned long long) * INPUT_MAX_GRID));
   n->n_counts = 2 * n_convs;
   if ((r = dalloc(n, &n->counts, sizeof(int) * std::max(1, n->n_counts)))) return r;
   CUDA_TRY(cudaMemset(n->first, 1, S));
@@ -988,6 +993,13 @@ dcnn_status dcnn_get_stats(dcnn_net* n, dcnn_op_stats* per_op, int64_t* frame_in
   const int L = (int)n->ops.size();
   std::vector<unsigned long long> raw((size_t)8 * (L + 1));
   CUDA_TRY(cudaMemcpy(raw.data(), n->stats, raw.size() * 8, cudaMemcpyDeviceToHost));
+  {
+    std::vector<unsigned long long> ca(INPUT_MAX_GRID);
+    CUDA_TRY(cudaMemcpy(ca.data(), n->cta_active, ca.size() * 8, cudaMemcpyDeviceToHost));
+    unsigned long long t = 0;
+    for (auto v : ca) t += v;                      // CTAs beyond the grid stay 0
+    raw[1] = t;                                    // active input pixels of the latest frame
+  }
   long long fi = 0;
   CUDA_TRY(cudaMemcpy(&fi, n->frame_idx, sizeof(long long), cudaMemcpyDeviceToHost));
   const int err = *(volatile int*)n->err_host;

@@ -98,14 +98,12 @@ __global__ void __launch_bounds__(256) k_input(InputParams p) {
     }
     __syncthreads();
   }
-  const int lane = tid & 31;
-  unsigned n = (unsigned)warp_sum((int)nact);
-  warp_count_flush(p.n_active, lane, n);
+  input_frame_counters(p.zero_stats, p.n_zero_stats, p.zero_counts, p.n_zero_counts, p.cta_active, nact);
 }
 
 void launch_input(const InputParams& p, int dtype, cudaStream_t st) {
   const int tiles = p.S * ((p.H + IN_TS - 1) / IN_TS) * ((p.W + IN_TS - 1) / IN_TS);
-  const int grid = tiles < 148 * 8 ? tiles : 148 * 8;
+  const int grid = tiles < INPUT_MAX_GRID ? tiles : INPUT_MAX_GRID;
   if (dtype == 1) launch_k(k_input<__half>, dim3(grid), dim3(256), 0, st, 1, p);
   else launch_k(k_input<float>, dim3(grid), dim3(256), 0, st, 1, p);
 }

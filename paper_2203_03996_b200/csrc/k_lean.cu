@@ -62,15 +62,13 @@ __global__ void __launch_bounds__(256) k_input_r0(InputParams p) {
     }
   }
   if (bad) atomicOr(p.err, 1);
-  const int lane = threadIdx.x & 31;
-  unsigned n = (unsigned)warp_sum((int)nact);
-  warp_count_flush(p.n_active, lane, n);
+  input_frame_counters(p.zero_stats, p.n_zero_stats, p.zero_counts, p.n_zero_counts, p.cta_active, nact);
 }
 
 void launch_input_r0(const InputParams& p, int dtype, cudaStream_t st) {
   const long long npix = (long long)p.S * p.H * p.W;
   long long blocks = (npix + 255) / 256;
-  const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
+  const int grid = (int)(blocks < INPUT_MAX_GRID ? blocks : INPUT_MAX_GRID);
   if (dtype == 1) launch_k(k_input_r0<__half>, dim3(grid), dim3(256), 0, st, 1, p);
   else launch_k(k_input_r0<float>, dim3(grid), dim3(256), 0, st, 1, p);
 }

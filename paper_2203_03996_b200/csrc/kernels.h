@@ -24,8 +24,13 @@ struct InputParams {
   uint8_t* first;               // [S] out: this frame's first-frame flags (copied from pend)
   const uint8_t* pend;          // [S] first-frame pending (set at create / by dcnn_reset)
   int* err;                     // sticky error word (bit 0: non-finite input)
-  unsigned long long* n_active;
+  unsigned long long* cta_active;  // [grid] active input pixels counted by each CTA (written, not added)
+  // per-frame counter reset folded into this first kernel: every later kernel adds to its
+  // counters only after its PDL wait, i.e. after this grid has finished
+  unsigned long long* zero_stats; int n_zero_stats;
+  int* zero_counts; int n_zero_counts;
 };
+constexpr int INPUT_MAX_GRID = 148 * 16;
 void launch_input(const InputParams& p, int dtype, cudaStream_t st);
 
 // ---------------------------------------------------------------- a2: tiles
