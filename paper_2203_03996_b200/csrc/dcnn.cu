@@ -456,6 +456,7 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
         if (lean_pool) launch_maxpool_disj(pp, n->cache32, ost);       // pool + A update, one launch
         else if (win_pool) launch_maxpool_win(pp, n->cache32, ost);     // pool, then A update
         else if (lean_up_ok(pp, n->dtype)) launch_up_lean(pp, ost);
+        else if (lean_add_ok(pp, n->dtype)) launch_add_lean(pp, n->cache32, ost);
         else launch_pointwise(pp, n->dtype, n->cache32, ost);
       }
       k += win_pool ? 2 : 1;

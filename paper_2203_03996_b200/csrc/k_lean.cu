@@ -15,6 +15,18 @@
 
 namespace dcnn {
 
+static int lean_grid(long long items) {
+  long long blocks = (items + 255) / 256;
+  return (int)(blocks < 1 ? 1 : (blocks < 148 * 16 ? blocks : 148 * 16));
+}
+
+static int log2_exact(int v) {
+  int l = 0;
+  while ((1 << l) < v) ++l;
+  return (1 << l) == v ? l : -1;
+}
+
+
 // ---------------------------------------------------------------- a1, r = 0
 // PAPER.md:129 "Delta Generation subtracts the previous input from the current";
 // m = [max_c |F - P| > eps_in] (strict, Z1); on m: delta = F - P, P := F.  First frame:
@@ -304,6 +316,119 @@ __global__ void __launch_bounds__(256) k_up_lean(PwParams p, int lg_nch) {
   warp_count_flush(p.ep.n_active, lane, n);
 }
 
+// ---------------------------------------------------------------- a6 + a5: add (+ activation)
+// Residual / fuse sums (HRNet: 131 per frame, most followed by ReLU truncation).  Thread =
+// (pixel, 8-channel chunk), G = C/8 consecutive lanes per pixel (power of two <= 32).  The
+// operands' masks and deltas and the pixel's x^A, x^T are all loaded at once; Z10: mask
+// union, an absent operand contributes 0 (select, so a stale delta is never used).  With an
+// activation, Eqs. 4-6 with the max-norm over the pixel's lanes (shuffle reduction).
+template <typename TC, int ACT>
+__global__ void __launch_bounds__(256) k_add_lean(PwParams p, int lg_nch) {
+  pdl_trigger();
+  pdl_wait();
+  frame_bookkeeping(p.ep);
+  const Epi& e = p.ep;
+  const int C = e.C, nch = 1 << lg_nch;
+  const long long npix = (long long)p.S * p.H * p.W;
+  const long long HW = (long long)p.H * p.W;
+  constexpr bool trunc = ACT != ACT_NONE;
+  const float eps = *e.eps;
+  unsigned nact = 0;
+  // whole warps per pass (the max-norm shuffle needs every lane): the loop runs over the
+  // work padded to a multiple of 32; a pixel's G lanes are all valid or all padding
+  const long long total = npix << lg_nch, total_pad = (total + 31) & ~31ll;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total_pad;
+       g += (long long)gridDim.x * blockDim.x) {
+    const bool valid = g < total;
+    const long long q = valid ? g >> lg_nch : 0;
+    const int j = (int)(g & (nch - 1));
+    const int s = (int)(q / HW);
+    const bool first = e.first[s] != 0;
+    uint8_t mk[4];
+    float dv[4][8], a[8], t[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k >= p.n_in) break;
+      mk[k] = (first || !valid) ? (valid ? 1 : 0) : p.min[k][q];
+      ld8(reinterpret_cast<const __half*>(p.in[k]) + q * C + 8 * j, dv[k]);
+    }
+    if (trunc && !first && valid) {
+      ld8(reinterpret_cast<const TC*>(e.xA) + q * C + 8 * j, a);
+      ld8(reinterpret_cast<const TC*>(e.xT) + q * C + 8 * j, t);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) a[c] = t[c] = 0.f;
+    }
+    bool on = false;
+    float z[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) z[c] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k >= p.n_in) break;
+      on |= mk[k] != 0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) z[c] += mk[k] ? dv[k][c] : 0.f;
+    }
+    bool upd = on;
+    float d[8];
+    if (trunc) {
+      float mx = 0.f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float prev = first ? 0.f : act_t<ACT>(a[c], e.act_param);
+        d[c] = act_t<ACT>(a[c] + t[c] + z[c], e.act_param) - prev;   // Eq. 5
+        mx = fmaxf(mx, fabsf(d[c]));
+      }
+      for (int o = nch >> 1; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      upd = on && (first || eps < 0.f || mx > eps);                  // strict rule (Z1)
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) d[c] = z[c];
+    }
+    if (upd) {
+      float o8[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) o8[c] = rnd<__half>(d[c]);
+      st8(reinterpret_cast<__half*>(e.delta) + q * C + 8 * j, o8);
+      if (trunc) {
+        float sv[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) sv[c] = a[c] + t[c] + z[c];
+        st8(reinterpret_cast<TC*>(e.xA) + q * C + 8 * j, sv);       // Eq. 6
+        st8_zero(reinterpret_cast<TC*>(e.xT) + q * C + 8 * j);
+      }
+    } else if (trunc && on) {
+      float tv[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) tv[c] = t[c] + z[c];
+      st8(reinterpret_cast<TC*>(e.xT) + q * C + 8 * j, tv);         // x^T += dx
+    }
+    if (j == 0 && valid) {
+      e.mask[q] = upd ? 1 : 0;
+      if (upd) ++nact;
+    }
+  }
+  const int lane = threadIdx.x & 31;
+  unsigned n = (unsigned)warp_sum((int)nact);
+  warp_count_flush(e.n_active, lane, n);
+}
+
+bool lean_add_ok(const PwParams& p, int dtype) {
+  return dtype == 1 && p.kind == 5 && p.n_in >= 1 && p.n_in <= 4 && p.ep.C % 8 == 0 && p.ep.C / 8 <= 32 &&
+         log2_exact(p.ep.C / 8) >= 0 && p.ep.O == nullptr;
+}
+
+void launch_add_lean(const PwParams& p, int cache32, cudaStream_t st) {
+  const int lg = log2_exact(p.ep.C / 8);
+  const int grid = lean_grid(((long long)p.S * p.H * p.W) << lg);
+  act_dispatch(p.ep.act, [&](auto A) {
+    constexpr int ACT = decltype(A)::value;
+    if (cache32) launch_k(k_add_lean<float, ACT>, dim3(grid), dim3(256), 0, st, 1, p, lg);
+    else launch_k(k_add_lean<__half, ACT>, dim3(grid), dim3(256), 0, st, 1, p, lg);
+  });
+}
+
 // ---------------------------------------------------------------- outputs to the caller
 __global__ void __launch_bounds__(256) k_copy_out(OutCopyParams p) {
   pdl_trigger();
@@ -330,17 +455,6 @@ __global__ void __launch_bounds__(256) k_copy_out(OutCopyParams p) {
 
 void launch_copy_out(const OutCopyParams& p, cudaStream_t st) {
   launch_k(k_copy_out, dim3(148 * 4), dim3(256), 0, st, 1, p);
-}
-
-static int lean_grid(long long items) {
-  long long blocks = (items + 255) / 256;
-  return (int)(blocks < 1 ? 1 : (blocks < 148 * 16 ? blocks : 148 * 16));
-}
-
-static int log2_exact(int v) {
-  int l = 0;
-  while ((1 << l) < v) ++l;
-  return (1 << l) == v ? l : -1;
 }
 
 bool lean_pool_ok(const PwParams& p, int dtype) {
