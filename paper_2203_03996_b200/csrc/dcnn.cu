@@ -457,6 +457,7 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
         else if (win_pool) launch_maxpool_win(pp, n->cache32, ost);     // pool, then A update
         else if (lean_up_ok(pp, n->dtype)) launch_up_lean(pp, ost);
         else if (lean_add_ok(pp, n->dtype)) launch_add_lean(pp, n->cache32, ost);
+        else if (lean_concat_ok(pp, n->dtype)) launch_concat_lean(pp, ost);
         else launch_pointwise(pp, n->dtype, n->cache32, ost);
       }
       k += win_pool ? 2 : 1;

@@ -429,6 +429,59 @@ void launch_add_lean(const PwParams& p, int cache32, cudaStream_t st) {
   });
 }
 
+// ---------------------------------------------------------------- a6: concat
+// Thread = (pixel, 8-channel chunk of the output).  Z10: output mask = union of the operand
+// masks; the channels of an operand whose mask bit is 0 are zero-filled.  Every operand mask
+// and the chunk's delta are loaded at once (one round trip).
+__global__ void __launch_bounds__(256) k_concat_lean(PwParams p, int nch) {
+  pdl_trigger();
+  pdl_wait();
+  frame_bookkeeping(p.ep);
+  const Epi& e = p.ep;
+  const int C = e.C;
+  const long long npix = (long long)p.S * p.H * p.W;
+  const long long HW = (long long)p.H * p.W;
+  unsigned nact = 0;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < npix * nch;
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long q = g / nch;
+    const int j = (int)(g - q * nch);
+    const bool first = e.first[q / HW] != 0;
+    int k = 0, off = 0;                        // operand owning channels [8j, 8j + 8)
+    while (k + 1 < p.n_in && 8 * j >= off + p.Cin[k]) { off += p.Cin[k]; ++k; }
+    uint8_t mk[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mk[i] = (i < p.n_in && !first) ? p.min[i][q] : (i < p.n_in ? 1 : 0);
+    const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(p.in[k]) + q * p.Cin[k] +
+                                                    (8 * j - off));
+    const bool mine = k == 0 ? mk[0] : k == 1 ? mk[1] : k == 2 ? mk[2] : mk[3];
+    const bool on = (mk[0] | mk[1] | mk[2] | mk[3]) != 0;
+    if (on)
+      *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.delta) + q * C + 8 * j) =
+          mine ? v : make_uint4(0u, 0u, 0u, 0u);
+    if (j == 0) {
+      e.mask[q] = on ? 1 : 0;
+      if (on) ++nact;
+    }
+  }
+  const int lane = threadIdx.x & 31;
+  unsigned n = (unsigned)warp_sum((int)nact);
+  warp_count_flush(e.n_active, lane, n);
+}
+
+bool lean_concat_ok(const PwParams& p, int dtype) {
+  if (dtype != 1 || p.kind != 6 || p.n_in < 1 || p.n_in > 4 || p.ep.O != nullptr || p.ep.act != 0) return false;
+  for (int k = 0; k < p.n_in; ++k)
+    if (p.Cin[k] % 8) return false;
+  return true;
+}
+
+void launch_concat_lean(const PwParams& p, cudaStream_t st) {
+  const int nch = p.ep.C / 8;
+  const int grid = lean_grid((long long)p.S * p.H * p.W * nch);
+  launch_k(k_concat_lean, dim3(grid), dim3(256), 0, st, 1, p, nch);
+}
+
 // ---------------------------------------------------------------- outputs to the caller
 __global__ void __launch_bounds__(256) k_copy_out(OutCopyParams p) {
   pdl_trigger();

@@ -134,6 +134,8 @@ bool lean_pool_win_ok(const PwParams& p, int dtype);   // 3x3 / 5x5 max-pool (ov
 void launch_maxpool_win(const PwParams& p, int cache32, cudaStream_t st);    // pool, then A update
 bool lean_add_ok(const PwParams& p, int dtype);        // add (+ act), fp16, C/8 power of 2 <= 32
 void launch_add_lean(const PwParams& p, int cache32, cudaStream_t st);
+bool lean_concat_ok(const PwParams& p, int dtype);     // concat, fp16, operand channels % 8 == 0
+void launch_concat_lean(const PwParams& p, cudaStream_t st);
 bool lean_up_ok(const PwParams& p, int dtype);         // nearest upsample, fp16, C/8 power of 2
 void launch_up_lean(const PwParams& p, cudaStream_t st);
 
