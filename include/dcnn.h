@@ -207,7 +207,9 @@ DCNN_API dcnn_status dcnn_debug_launch_times(dcnn_net* net, int32_t max, int32_t
  * that any read of a masked-off (stale) value would surface in the outputs. */
 DCNN_API dcnn_status dcnn_debug_poison(dcnn_net* net);
 
-/* Debug timeline of the tensor-core conv kernel: when a net is created with the
+/* Debug timeline of the tensor-core conv kernel (trace build only: compile with
+ * DCNN_EXTRA_NVCC_FLAGS=-DDCNN_TRACE; the normal build keeps its hot paths free of the
+ * stamps and this table stays zero).  When a net is created with the
  * environment variable DCNN_TC_DBG=4, CTA 0 of every tcgen05 conv launch writes
  * %globaltimer stamps (ns) of its pipeline milestones into a process-wide table of
  * 32 slots; this copies the table (of the latest launch) to host32[32].  Syncs the

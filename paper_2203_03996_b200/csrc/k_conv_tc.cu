@@ -81,8 +81,14 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+#ifdef DCNN_TRACE    // trace build only (tools/trace_tc.py): keeps the hot paths free of the stamps
 #define TCTR(cond, slot) \
   do { if ((p.dbg & 4) && blockIdx.x == 0 && (cond)) g_tc_trace[slot] = gtime(); } while (0)
+#define TC_DBG(bit) (p.dbg & (bit))
+#else
+#define TCTR(cond, slot) do { } while (0)
+#define TC_DBG(bit) false
+#endif
 
 // 4-D TMA tile load global -> shared, completion counted on an mbarrier (transaction bytes)
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       const uint8_t* hm = smem + L.hmask + pg_slot * TC_HMASK_BYTES;
       unsigned char* A = smem + L.a0 + b * p.a_bytes;
       int hy = hy_0, hx = hx_0;
-      for (int px = (p.dbg & 8) ? npx : lt; px < npx; px += 32) {   // dbg 8: no zero pass (timing only)
+      for (int px = TC_DBG(8) ? npx : lt; px < npx; px += 32) {   // dbg 8: no zero pass (trace build, timing only)
         const int iy = pg_iy0 + hy, ix = pg_ix0 + hx;
         if (!hm[px] && iy >= 0 && iy < p.H && ix >= 0 && ix < p.W) {
           if (p.sw128) {                       // the pixel's whole 128-B row (swizzle permutes within it)
@@ -384,7 +390,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         const int s = tile / (p.nty * p.ntx);
         const int ty = (tile / p.ntx) % p.nty, tx = tile % p.ntx;
         const int iy0 = ty * 16 * p.stride - p.pad, ix0 = tx * 8 * p.stride - p.pad;
-        if (p.dbg & 16) { tc::mbar_arrive(&a_tma[b]); return; }   // dbg 16: no halo copies (timing only)
+        if (TC_DBG(16)) { tc::mbar_arrive(&a_tma[b]); return; }   // dbg 16: no halo copies (trace build)
         tc::mbar_arrive_expect_tx(&a_tma[b], gbytes);
         const uint32_t A = tc::smem_u32(smem + L.a0 + b * p.a_bytes);
         if (p.sw128) {                         // one box: 64 channels x 8 columns x 16 rows, swizzled
@@ -517,7 +523,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
               }
             }
             if (!p.resident) {
-              if (p.dbg & 64) tc::mbar_arrive(&b_empty[st]);   // dbg 64: release early (timing only)
+              if (TC_DBG(64)) tc::mbar_arrive(&b_empty[st]);   // dbg 64: release early (trace build)
               else tc::mma_commit(&b_empty[st]);               // stage reusable once these finish
             }
           }

@@ -1,4 +1,7 @@
-"""Pipeline timeline of the tcgen05 conv (CTA 0) for single-conv nets: run with DCNN_TC_DBG=4."""
+"""Pipeline timeline of the tcgen05 conv (CTA 0) for single-conv nets: run with DCNN_TC_DBG=4
+against a trace build of the library:
+    DCNN_EXTRA_NVCC_FLAGS=-DDCNN_TRACE DCNN_BUILD_SUFFIX=_trace python -m paper_2203_03996_b200.build
+    DCNN_LIB=paper_2203_03996_b200/libdcnn_trace.so python tools/trace_tc.py [H,W,Ci,Co,k,s ...]"""
 import os, sys
 os.environ.setdefault("DCNN_TC_DBG", "4")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
