@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   if (warp == 9) {
     // A-operand start offset of every tap inside a halo buffer: phase (kx*d) mod s,
     // row ky*d, column of the phase (kx*d) div s
+#pragma unroll 1
     for (int t = lane; t < ntaps; t += 32) {
       const int ky = t / p.kw, kx = t - (t / p.kw) * p.kw;
       const int xo = kx * p.dil;
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   const int npre = p.resident ? nsteps : (p.stages < nsteps ? p.stages : nsteps);
   if (warp == 9) {
     if (tc::elect_one()) {
+#pragma unroll 1
       for (int st = 0; st < npre; ++st) {
         tc::mbar_arrive_expect_tx(&b_full[st], p.b_bytes);
         tc::bulk_g2s(bstage + (size_t)st * p.b_bytes, wsrc + (size_t)st * p.b_bytes, p.b_bytes, &b_full[st]);
@@ -226,6 +228,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const int npx = p.HH * p.WW;
     const int hy_0 = lane / p.WW, hx_0 = lane - hy_0 * p.WW, dy32 = 32 / p.WW, dx32 = 32 - dy32 * p.WW;
     uint32_t kxmask = 0;                       // column offsets of the taps
+#pragma unroll 1
     for (int kx = 0; kx < p.kw; ++kx) kxmask |= 1u << (kx * p.dil);
     unsigned long long n_tot = 0, n_skip = 0, n_dense = 0, n_mc = 0;
     int v = 0;
@@ -398,7 +401,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           return;
         }
         // one box of 8 channels x (columns of one stride phase) x halo rows per plane
+#pragma unroll 1
         for (int ph = 0; ph < p.stride; ++ph)
+#pragma unroll 1
           for (int ch = 0; ch < nch; ++ch)
             tma_load_4d(A + ph * p.phase_bytes + ch * p.plane, &p.tmap, cb * p.BK + ch * 8, ix0 + ph, iy0, s,
                         &a_tma[b]);
