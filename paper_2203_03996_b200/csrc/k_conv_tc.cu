@@ -796,14 +796,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         if (coal && ((c0 & 31) == 24 || c0 + 8 >= C)) {   // slice complete: flush
           const int sl = c0 & ~31, n16 = n16_of(sl);
           TCTR(tid == 0 && u == 0 && sl == 0, 19);
-          if (trunc) {
-            stage_move(SA, gA + sl, n16, updm, 1);
-            TCTR(tid == 0 && u == 0 && sl == 0, 20);
-            // x^T := x^T + dx where truncated; := 0 where updated and it was pending
-            stage_move(ST, gT + sl, n16, (actm & ~updm) | (updm & tm), 1, updm);
+          // x^A where updated; x^T := x^T + dx where truncated, := 0 where updated and pending;
+          // the delta where updated -- one (rolled) call site keeps the code short
+#pragma unroll 1
+          for (int w = trunc ? 0 : 2; w < 3; ++w) {
+            unsigned char* area = w == 0 ? SA : w == 1 ? ST : SD;
+            __half* gb = (w == 0 ? gA : w == 1 ? gT : gD) + sl;
+            const uint32_t pm = w == 1 ? ((actm & ~updm) | (updm & tm)) : updm;
+            stage_move(area, gb, n16, pm, 1, w == 1 ? updm : 0u);
           }
-          TCTR(tid == 0 && u == 0 && sl == 0, 21);
-          stage_move(SD, gD + sl, n16, updm, 1);
           TCTR(tid == 0 && u == 0 && sl == 0, 22);
           if (O && updm) {
             // a8 (output accumulation) O += delta for the slice, coalesced: 8 lanes per pixel
