@@ -331,7 +331,8 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
   ip.zero_counts = n->counts; ip.n_zero_counts = n->n_counts;
   {
     TimeScope ts(n, st, DCNN_KCLASS_INPUT);
-    if (ip.radius == 0 && ip.C <= 4) launch_input_r0(ip, n->dtype, st);
+    if (ip.radius == 0 && ip.C <= 4 && (long long)ip.S * ip.H * ip.W < (1ll << 30))   // 32-bit index math
+      launch_input_r0(ip, n->dtype, st);
     else launch_input(ip, n->dtype, st);
   }
   ++k;

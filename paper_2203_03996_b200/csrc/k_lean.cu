@@ -35,8 +35,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_input_r0(InputParams p) {
   pdl_trigger();
   pdl_wait();
-  const long long npix = (long long)p.S * p.H * p.W;
-  const long long HW = (long long)p.H * p.W;
+  const int npix = p.S * p.H * p.W;   // < 2^31 (host-checked): 32-bit index math
+  const int HW = p.H * p.W;
   const T* F = reinterpret_cast<const T*>(p.frame);
   T* P = reinterpret_cast<T*>(p.P);
   T* D = reinterpret_cast<T*>(p.delta);
@@ -44,17 +44,16 @@ __global__ void __launch_bounds__(256) k_input_r0(InputParams p) {
   const int C = p.C;
   unsigned nact = 0;
   bool bad = false;
-  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < npix;
-       q += (long long)gridDim.x * blockDim.x) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < npix; q += gridDim.x * blockDim.x) {
     const int s = (int)(q / HW);
     float f[4], pv[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      f[c] = c < C ? ld(F + q * C + c) : 0.f;
-      pv[c] = c < C ? ld(P + q * C + c) : 0.f;
+      f[c] = c < C ? ld(F + (long long)q * C + c) : 0.f;
+      pv[c] = c < C ? ld(P + (long long)q * C + c) : 0.f;
     }
     const bool first = p.pend[s] != 0;
-    if (q == (long long)s * HW) p.first[s] = first ? 1 : 0;        // this frame's flag
+    if (q == s * HW) p.first[s] = first ? 1 : 0;        // this frame's flag
     float mx = 0.f;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -68,8 +67,8 @@ __global__ void __launch_bounds__(256) k_input_r0(InputParams p) {
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         if (c < C) {
-          st(D + q * p.Cp + c, first ? f[c] : f[c] - pv[c]);
-          st(P + q * C + c, f[c]);
+          st(D + (long long)q * p.Cp + c, first ? f[c] : f[c] - pv[c]);
+          st(P + (long long)q * C + c, f[c]);
         }
     }
   }
@@ -94,18 +93,17 @@ __global__ void __launch_bounds__(256) k_maxpool_disj(PwParams p, int lg_nch) {
   frame_bookkeeping(p.ep);
   constexpr int k = KK;
   const int C = p.ep.C, nch = 1 << lg_nch;
-  const long long nout = (long long)p.S * p.H * p.W;
-  const long long HWo = (long long)p.H * p.W;
+  const int nout = p.S * p.H * p.W;   // < 2^31 (host-checked): 32-bit index math
+  const int HWo = p.H * p.W;
   const T* din = reinterpret_cast<const T*>(p.in[0]);
   T* dout = reinterpret_cast<T*>(p.ep.delta);
   TC* A = reinterpret_cast<TC*>(p.poolA);
   unsigned nact = 0;
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < (nout << lg_nch);
-       g += (long long)gridDim.x * blockDim.x) {
-    const long long q = g >> lg_nch;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < (nout << lg_nch); g += gridDim.x * blockDim.x) {
+    const int q = g >> lg_nch;
     const int j = (int)(g & (nch - 1));
     const int s = (int)(q / HWo);
-    const int rem = (int)(q - (long long)s * HWo);
+    const int rem = q - s * HWo;
     const int y = rem / p.W, x = rem - (rem / p.W) * p.W;
     const long long ibase = ((long long)s * p.Hi + (long long)y * k) * p.Wi + (long long)x * k;
     const bool first = p.ep.first[s] != 0;
@@ -141,9 +139,9 @@ __global__ void __launch_bounds__(256) k_maxpool_disj(PwParams p, int lg_nch) {
       float o[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) o[c] = rnd<T>(first ? mnew[c] : mnew[c] - mold[c]);   // Eq. 3
-      st8(dout + q * C + 8 * j, o);
+      st8(dout + (long long)q * C + 8 * j, o);
       if (p.ep.O) {
-        float* O = p.ep.O + q * C + 8 * j;
+        float* O = p.ep.O + (long long)q * C + 8 * j;
         float ov[8];
         if (first) {
 #pragma unroll
@@ -179,18 +177,17 @@ __global__ void __launch_bounds__(256) k_maxpool_win(PwParams p, int lg_nch) {
   pdl_wait();
   frame_bookkeeping(p.ep);
   const int C = p.ep.C, nch = 1 << lg_nch;
-  const long long nout = (long long)p.S * p.H * p.W;
-  const long long HWo = (long long)p.H * p.W;
+  const int nout = p.S * p.H * p.W;   // < 2^31 (host-checked): 32-bit index math
+  const int HWo = p.H * p.W;
   const T* din = reinterpret_cast<const T*>(p.in[0]);
   T* dout = reinterpret_cast<T*>(p.ep.delta);
   const TC* A = reinterpret_cast<const TC*>(p.poolA);
   unsigned nact = 0;
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < (nout << lg_nch);
-       g += (long long)gridDim.x * blockDim.x) {
-    const long long q = g >> lg_nch;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < (nout << lg_nch); g += gridDim.x * blockDim.x) {
+    const int q = g >> lg_nch;
     const int j = (int)(g & (nch - 1));
     const int s = (int)(q / HWo);
-    const int rem = (int)(q - (long long)s * HWo);
+    const int rem = q - s * HWo;
     const int y = rem / p.W, x = rem - (rem / p.W) * p.W;
     const long long sbase = (long long)s * p.Hi * p.Wi;
     const bool first = p.ep.first[s] != 0;
@@ -233,9 +230,9 @@ __global__ void __launch_bounds__(256) k_maxpool_win(PwParams p, int lg_nch) {
       float o[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) o[c] = rnd<T>(first ? mnew[c] : mnew[c] - mold[c]);   // Eq. 3
-      st8(dout + q * C + 8 * j, o);
+      st8(dout + (long long)q * C + 8 * j, o);
       if (p.ep.O) {
-        float* O = p.ep.O + q * C + 8 * j;
+        float* O = p.ep.O + (long long)q * C + 8 * j;
         float ov[8];
         if (first) {
 #pragma unroll
@@ -261,23 +258,22 @@ __global__ void __launch_bounds__(256) k_pool_update_vec(PwParams p, int lg_nch)
   pdl_trigger();
   pdl_wait();
   const int C = p.ep.C, nch = 1 << lg_nch;
-  const long long HWi = (long long)p.Hi * p.Wi;
-  const long long npx = (long long)p.S * HWi;
+  const int HWi = p.Hi * p.Wi;
+  const int npx = p.S * HWi;
   const T* d = reinterpret_cast<const T*>(p.in[0]);
   TC* A = reinterpret_cast<TC*>(p.poolA);
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < (npx << lg_nch);
-       g += (long long)gridDim.x * blockDim.x) {
-    const long long q = g >> lg_nch;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < (npx << lg_nch); g += gridDim.x * blockDim.x) {
+    const int q = g >> lg_nch;
     const int j = (int)(g & (nch - 1));
     const bool first = p.ep.first[q / HWi] != 0;
     const uint8_t m = p.min[0][q];
     float dv[8], av[8];
-    ld8(d + q * C + 8 * j, dv);
-    if (!first) ld8(A + q * C + 8 * j, av);
+    ld8(d + (long long)q * C + 8 * j, dv);
+    if (!first) ld8(A + (long long)q * C + 8 * j, av);
     if (first || m) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) av[c] = (first ? 0.f : av[c]) + dv[c];
-      st8(A + q * C + 8 * j, av);
+      st8(A + (long long)q * C + 8 * j, av);
     }
   }
 }
@@ -289,17 +285,16 @@ __global__ void __launch_bounds__(256) k_up_lean(PwParams p, int lg_nch) {
   pdl_wait();
   frame_bookkeeping(p.ep);
   const int C = p.ep.C, nch = 1 << lg_nch, f = p.up;
-  const long long nout = (long long)p.S * p.H * p.W;
-  const long long HWo = (long long)p.H * p.W;
+  const int nout = p.S * p.H * p.W;   // < 2^31 (host-checked): 32-bit index math
+  const int HWo = p.H * p.W;
   const T* din = reinterpret_cast<const T*>(p.in[0]);
   T* dout = reinterpret_cast<T*>(p.ep.delta);
   unsigned nact = 0;
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < (nout << lg_nch);
-       g += (long long)gridDim.x * blockDim.x) {
-    const long long q = g >> lg_nch;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < (nout << lg_nch); g += gridDim.x * blockDim.x) {
+    const int q = g >> lg_nch;
     const int j = (int)(g & (nch - 1));
     const int s = (int)(q / HWo);
-    const int rem = (int)(q - (long long)s * HWo);
+    const int rem = q - s * HWo;
     const int y = rem / p.W, x = rem - (rem / p.W) * p.W;
     const long long ip = ((long long)s * p.Hi + y / f) * p.Wi + x / f;
     const uint8_t m = p.min[0][ip];
@@ -307,7 +302,7 @@ __global__ void __launch_bounds__(256) k_up_lean(PwParams p, int lg_nch) {
     const bool on = p.ep.first[s] != 0 || m;
     if (j == 0) p.ep.mask[q] = on ? 1 : 0;
     if (on) {
-      *reinterpret_cast<uint4*>(dout + q * C + 8 * j) = v;
+      *reinterpret_cast<uint4*>(dout + (long long)q * C + 8 * j) = v;
       if (j == 0) ++nact;
     }
   }
@@ -329,18 +324,17 @@ __global__ void __launch_bounds__(256) k_add_lean(PwParams p, int lg_nch) {
   frame_bookkeeping(p.ep);
   const Epi& e = p.ep;
   const int C = e.C, nch = 1 << lg_nch;
-  const long long npix = (long long)p.S * p.H * p.W;
-  const long long HW = (long long)p.H * p.W;
+  const int npix = p.S * p.H * p.W;   // < 2^31 (host-checked): 32-bit index math
+  const int HW = p.H * p.W;
   constexpr bool trunc = ACT != ACT_NONE;
   const float eps = *e.eps;
   unsigned nact = 0;
   // whole warps per pass (the max-norm shuffle needs every lane): the loop runs over the
   // work padded to a multiple of 32; a pixel's G lanes are all valid or all padding
-  const long long total = npix << lg_nch, total_pad = (total + 31) & ~31ll;
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total_pad;
-       g += (long long)gridDim.x * blockDim.x) {
+  const int total = npix << lg_nch, total_pad = (total + 31) & ~31;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total_pad; g += gridDim.x * blockDim.x) {
     const bool valid = g < total;
-    const long long q = valid ? g >> lg_nch : 0;
+    const int q = valid ? g >> lg_nch : 0;
     const int j = (int)(g & (nch - 1));
     const int s = (int)(q / HW);
     const bool first = e.first[s] != 0;
@@ -350,11 +344,11 @@ __global__ void __launch_bounds__(256) k_add_lean(PwParams p, int lg_nch) {
     for (int k = 0; k < 4; ++k) {
       if (k >= p.n_in) break;
       mk[k] = (first || !valid) ? (valid ? 1 : 0) : p.min[k][q];
-      ld8(reinterpret_cast<const __half*>(p.in[k]) + q * C + 8 * j, dv[k]);
+      ld8(reinterpret_cast<const __half*>(p.in[k]) + (long long)q * C + 8 * j, dv[k]);
     }
     if (trunc && !first && valid) {
-      ld8(reinterpret_cast<const TC*>(e.xA) + q * C + 8 * j, a);
-      ld8(reinterpret_cast<const TC*>(e.xT) + q * C + 8 * j, t);
+      ld8(reinterpret_cast<const TC*>(e.xA) + (long long)q * C + 8 * j, a);
+      ld8(reinterpret_cast<const TC*>(e.xT) + (long long)q * C + 8 * j, t);
     } else {
 #pragma unroll
       for (int c = 0; c < 8; ++c) a[c] = t[c] = 0.f;
@@ -390,19 +384,19 @@ __global__ void __launch_bounds__(256) k_add_lean(PwParams p, int lg_nch) {
       float o8[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) o8[c] = rnd<__half>(d[c]);
-      st8(reinterpret_cast<__half*>(e.delta) + q * C + 8 * j, o8);
+      st8(reinterpret_cast<__half*>(e.delta) + (long long)q * C + 8 * j, o8);
       if (trunc) {
         float sv[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) sv[c] = a[c] + t[c] + z[c];
-        st8(reinterpret_cast<TC*>(e.xA) + q * C + 8 * j, sv);       // Eq. 6
-        st8_zero(reinterpret_cast<TC*>(e.xT) + q * C + 8 * j);
+        st8(reinterpret_cast<TC*>(e.xA) + (long long)q * C + 8 * j, sv);       // Eq. 6
+        st8_zero(reinterpret_cast<TC*>(e.xT) + (long long)q * C + 8 * j);
       }
     } else if (trunc && on) {
       float tv[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) tv[c] = t[c] + z[c];
-      st8(reinterpret_cast<TC*>(e.xT) + q * C + 8 * j, tv);         // x^T += dx
+      st8(reinterpret_cast<TC*>(e.xT) + (long long)q * C + 8 * j, tv);         // x^T += dx
     }
     if (j == 0 && valid) {
       e.mask[q] = upd ? 1 : 0;
@@ -414,8 +408,16 @@ __global__ void __launch_bounds__(256) k_add_lean(PwParams p, int lg_nch) {
   warp_count_flush(e.n_active, lane, n);
 }
 
+// The lean kernels index in 32 bits (64-bit division sequences are most of a small kernel's code,
+// and code size is latency at one stream): every grid-stride index must stay below 2^30.
+static bool fits32(const PwParams& p) {
+  const long long px = (long long)p.S * (p.H * (long long)p.W > p.Hi * (long long)p.Wi ? p.H * (long long)p.W
+                                                                                        : p.Hi * (long long)p.Wi);
+  return px * ((p.ep.C + 7) / 8) < (1ll << 30);
+}
+
 bool lean_add_ok(const PwParams& p, int dtype) {
-  return dtype == 1 && p.kind == 5 && p.n_in >= 1 && p.n_in <= 4 && p.ep.C % 8 == 0 && p.ep.C / 8 <= 32 &&
+  return fits32(p) && dtype == 1 && p.kind == 5 && p.n_in >= 1 && p.n_in <= 4 && p.ep.C % 8 == 0 && p.ep.C / 8 <= 32 &&
          log2_exact(p.ep.C / 8) >= 0 && p.ep.O == nullptr;
 }
 
@@ -439,12 +441,11 @@ __global__ void __launch_bounds__(256) k_concat_lean(PwParams p, int nch) {
   frame_bookkeeping(p.ep);
   const Epi& e = p.ep;
   const int C = e.C;
-  const long long npix = (long long)p.S * p.H * p.W;
-  const long long HW = (long long)p.H * p.W;
+  const int npix = p.S * p.H * p.W;   // < 2^31 (host-checked): 32-bit index math
+  const int HW = p.H * p.W;
   unsigned nact = 0;
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < npix * nch;
-       g += (long long)gridDim.x * blockDim.x) {
-    const long long q = g / nch;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < npix * nch; g += gridDim.x * blockDim.x) {
+    const int q = g / nch;
     const int j = (int)(g - q * nch);
     const bool first = e.first[q / HW] != 0;
     int k = 0, off = 0;                        // operand owning channels [8j, 8j + 8)
@@ -452,12 +453,12 @@ __global__ void __launch_bounds__(256) k_concat_lean(PwParams p, int nch) {
     uint8_t mk[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) mk[i] = (i < p.n_in && !first) ? p.min[i][q] : (i < p.n_in ? 1 : 0);
-    const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(p.in[k]) + q * p.Cin[k] +
+    const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(p.in[k]) + (long long)q * p.Cin[k] +
                                                     (8 * j - off));
     const bool mine = k == 0 ? mk[0] : k == 1 ? mk[1] : k == 2 ? mk[2] : mk[3];
     const bool on = (mk[0] | mk[1] | mk[2] | mk[3]) != 0;
     if (on)
-      *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.delta) + q * C + 8 * j) =
+      *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.delta) + (long long)q * C + 8 * j) =
           mine ? v : make_uint4(0u, 0u, 0u, 0u);
     if (j == 0) {
       e.mask[q] = on ? 1 : 0;
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(256) k_concat_lean(PwParams p, int nch) {
 }
 
 bool lean_concat_ok(const PwParams& p, int dtype) {
-  if (dtype != 1 || p.kind != 6 || p.n_in < 1 || p.n_in > 4 || p.ep.O != nullptr || p.ep.act != 0) return false;
+  if (!fits32(p) || dtype != 1 || p.kind != 6 || p.n_in < 1 || p.n_in > 4 || p.ep.O != nullptr || p.ep.act != 0) return false;
   for (int k = 0; k < p.n_in; ++k)
     if (p.Cin[k] % 8) return false;
   return true;
@@ -511,12 +512,12 @@ void launch_copy_out(const OutCopyParams& p, cudaStream_t st) {
 }
 
 bool lean_pool_ok(const PwParams& p, int dtype) {
-  return dtype == 1 && p.kind == 2 && p.k == 2 && p.stride == 2 && p.pad == 0 && p.Hi % p.k == 0 &&
+  return fits32(p) && dtype == 1 && p.kind == 2 && p.k == 2 && p.stride == 2 && p.pad == 0 && p.Hi % p.k == 0 &&
          p.Wi % p.k == 0 && p.ep.C % 8 == 0 && log2_exact(p.ep.C / 8) >= 0 && p.ep.act == 0;
 }
 
 bool lean_pool_win_ok(const PwParams& p, int dtype) {
-  return dtype == 1 && p.kind == 2 && (p.k == 5 || p.k == 3) && p.ep.C % 8 == 0 && log2_exact(p.ep.C / 8) >= 0 &&
+  return fits32(p) && dtype == 1 && p.kind == 2 && (p.k == 5 || p.k == 3) && p.ep.C % 8 == 0 && log2_exact(p.ep.C / 8) >= 0 &&
          p.ep.act == 0;
 }
 
@@ -536,7 +537,7 @@ void launch_maxpool_win(const PwParams& p, int cache32, cudaStream_t st) {
 }
 
 bool lean_up_ok(const PwParams& p, int dtype) {
-  return dtype == 1 && p.kind == 4 && p.ep.C % 8 == 0 && log2_exact(p.ep.C / 8) >= 0 && p.ep.O == nullptr &&
+  return fits32(p) && dtype == 1 && p.kind == 4 && p.ep.C % 8 == 0 && log2_exact(p.ep.C / 8) >= 0 && p.ep.O == nullptr &&
          p.ep.act == 0;
 }
 
