@@ -91,6 +91,7 @@ struct dcnn_net {
   // device state
   void* frame_in = nullptr;
   void* P = nullptr;
+  void* P1 = nullptr;               // second P buffer when the input mask is dilated (r > 0)
   void* in_delta = nullptr;
   uint8_t* in_mask = nullptr;
   uint8_t* first = nullptr;         // [S] this frame's first-frame flags (written by the input kernel)
@@ -324,7 +325,7 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
   const int nops = (int)n->ops.size();
   InputParams ip;
   ip.S = n->S; ip.H = n->inH; ip.W = n->inW; ip.C = n->inC; ip.Cp = n->inCp; ip.radius = n->radius;
-  ip.frame = n->frame_in; ip.P = n->P; ip.delta = n->in_delta; ip.mask = n->in_mask;
+  ip.frame = n->frame_in; ip.P = n->P; ip.P1 = n->P1; ip.frame_idx = n->frame_idx; ip.delta = n->in_delta; ip.mask = n->in_mask;
   ip.eps = n->eps; ip.first = n->first; ip.pend = n->pend; ip.err = n->err;
   ip.cta_active = n->cta_active;
   ip.zero_stats = n->stats + 8; ip.n_zero_stats = 8 * nops;   // slot 0 (the input) is per-CTA
@@ -712,6 +713,10 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   CUDA_TRY(cudaMemset(n->frame_idx, 0, S * sizeof(long long)));
 
   CUDA_TRY(cudaMemset(n->P, 0, n->frame_bytes));
+  if (n->radius > 0 && n->bookkeeper >= 0) {   // halo reads of P race with in-place updates
+    if ((r = dalloc(n, &n->P1, n->frame_bytes))) return r;
+    CUDA_TRY(cudaMemset(n->P1, 0, n->frame_bytes));
+  }
 
   n->eps_host.assign(L + 1, 0.f);
   n->eps_host[0] = d->input_threshold;
@@ -1054,7 +1059,23 @@ dcnn_status dcnn_debug_read(dcnn_net* n, int32_t op, int32_t which, void* host, 
         }
         return DCNN_OK;
       case DCNN_BUF_MASK: src = n->in_mask; nb = px; break;
-      case DCNN_BUF_XA: src = n->P; nb = px * n->inC * es; break;
+      case DCNN_BUF_XA:
+        src = n->P; nb = px * n->inC * es;
+        if (n->P1) {                   // per stream: the buffer the next frame reads
+          if (bytes) *bytes = (int64_t)nb;
+          if (host) {
+            CUDA_TRY(cudaDeviceSynchronize());
+            std::vector<long long> fi(n->S);
+            CUDA_TRY(cudaMemcpy(fi.data(), n->frame_idx, n->S * sizeof(long long), cudaMemcpyDeviceToHost));
+            const size_t sb = nb / n->S;
+            for (int s = 0; s < n->S; ++s)
+              CUDA_TRY(cudaMemcpy(static_cast<char*>(host) + s * sb,
+                                  static_cast<const char*>((fi[s] & 1) ? n->P1 : n->P) + s * sb, sb,
+                                  cudaMemcpyDeviceToHost));
+          }
+          return DCNN_OK;
+        }
+        break;
       default: return fail(DCNN_ERR_ARG, "buffer not present for the input layer");
     }
   } else {

@@ -29,7 +29,6 @@ __global__ void __launch_bounds__(256) k_input(InputParams p) {
   const int r = p.radius;
   const int HH = IN_TS + 2 * r, WH = IN_TS + 2 * r;
   const T* F = reinterpret_cast<const T*>(p.frame);
-  T* P = reinterpret_cast<T*>(p.P);
   T* D = reinterpret_cast<T*>(p.delta);
   const int C = p.C;
   unsigned nact = 0;
@@ -39,6 +38,9 @@ __global__ void __launch_bounds__(256) k_input(InputParams p) {
     const int tx = b % tiles_x;
     const bool first = p.pend[s] != 0;
     if (ty == 0 && tx == 0 && tid == 0) p.first[s] = first ? 1 : 0;   // this frame's flag
+    const bool odd = p.P1 && (p.frame_idx[s] & 1);
+    const T* P = reinterpret_cast<const T*>(odd ? p.P1 : p.P);        // read
+    T* Pw = reinterpret_cast<T*>(p.P1 ? (odd ? p.P : p.P1) : p.P);   // write
     const float eps = *p.eps;
     const bool all = first || eps < 0.f;
     const int y0 = ty * IN_TS - r, x0 = tx * IN_TS - r;
@@ -92,8 +94,135 @@ __global__ void __launch_bounds__(256) k_input(InputParams p) {
           const float f = ld(F + pix * C + c);
           const float d = first ? f : f - ld(P + pix * C + c);
           st(D + pix * p.Cp + c, d);
-          st(P + pix * C + c, f);
+          st(Pw + pix * C + c, f);
         }
+      } else if (p.P1) {
+        for (int c = 0; c < C; ++c) st(Pw + pix * C + c, ld(P + pix * C + c));
+      }
+    }
+    __syncthreads();
+  }
+  input_frame_counters(p.zero_stats, p.n_zero_stats, p.zero_counts, p.n_zero_counts, p.cta_active, nact);
+}
+
+// Few-channel frames (C <= 4, the RGB inputs of the HRNet / YOLOv5s workloads), 1 <= r <= 16.
+// Same arithmetic as k_input; the work is reorganised so the kernel is not instruction-bound
+// (the byte-per-pixel dilation passes were most of k_input's issue slots):
+//  * a warp thresholds two halo rows per step (lanes = columns hx and hx + 32, every load of the
+//    step in flight at once) and the row's mask bits are gathered with ballots into one 64-bit
+//    word per halo row;
+//  * the dilation is bitwise: OR of 2r+1 shifted row words, then OR of 2r+1 row words;
+//  * the core pixels' F and P stay in shared memory, so the emit pass only writes.
+template <typename T>
+__global__ void __launch_bounds__(256, 3) k_input_c4(InputParams p) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ unsigned long long rowbits[IN_TS + 2 * IN_RMAX];   // threshold bits per halo row
+  __shared__ uint32_t hdil[IN_TS + 2 * IN_RMAX];                // row-dilated core columns
+  __shared__ uint32_t cmask[IN_TS];                             // final mask per core row
+  __shared__ T fs[IN_TS * IN_TS * 4], ps[IN_TS * IN_TS * 4];    // core pixels' F and P
+  const int tiles_x = (p.W + IN_TS - 1) / IN_TS;
+  const int tiles_y = (p.H + IN_TS - 1) / IN_TS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = p.radius;
+  const int WH = IN_TS + 2 * r;
+  const T* F = reinterpret_cast<const T*>(p.frame);
+  T* D = reinterpret_cast<T*>(p.delta);
+  const int C = p.C;
+  const float eps = *p.eps;
+  unsigned nact = 0;
+  for (int b = blockIdx.x; b < p.S * tiles_y * tiles_x; b += gridDim.x) {
+    const int s = b / (tiles_y * tiles_x);
+    const int ty = (b / tiles_x) % tiles_y;
+    const int tx = b % tiles_x;
+    const bool first = p.pend[s] != 0;
+    if (ty == 0 && tx == 0 && tid == 0) p.first[s] = first ? 1 : 0;   // this frame's flag
+    const bool odd = p.frame_idx[s] & 1;                               // P double-buffered
+    const T* P = reinterpret_cast<const T*>(odd ? p.P1 : p.P);
+    T* Pw = reinterpret_cast<T*>(odd ? p.P : p.P1);
+    const bool all = first || eps < 0.f;
+    const int y0 = ty * IN_TS - r, x0 = tx * IN_TS - r;
+    const long long sbase = (long long)s * p.H * p.W;
+    bool bad = false;
+    // 1. threshold: warp w takes halo rows 2w, 2w+1, 2w+16, 2w+17, ...
+    for (int hb = 2 * warp; hb < WH; hb += 16) {
+      float f[4][4], pv[4][4];
+      bool in[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {                // u = (row offset, column half)
+        const int hy = hb + (u >> 1), hx = lane + 32 * (u & 1);
+        const int y = y0 + hy, x = x0 + hx;
+        in[u] = hy < WH && hx < WH && y >= 0 && y < p.H && x >= 0 && x < p.W;
+        // unconditional loads from a clamped in-bounds address, then a select: no branch per load
+        const int yc = min(max(y, 0), p.H - 1), xc = min(max(x, 0), p.W - 1);
+        const long long base = (sbase + (long long)yc * p.W + xc) * C;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const long long o = base + min(c, C - 1);
+          const float fr = ld(F + o), pr = ld(P + o);
+          f[u][c] = (in[u] && c < C) ? fr : 0.f;
+          pv[u][c] = (in[u] && c < C && !first) ? pr : 0.f;
+        }
+      }
+      uint32_t bits[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int hy = hb + (u >> 1), hx = lane + 32 * (u & 1);
+        float mx = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < C) mx = fmaxf(mx, fabsf(f[u][c] - pv[u][c]));
+        const bool v = in[u] && (all || mx > eps);   // strict (Z1)
+        bits[u] = __ballot_sync(0xffffffffu, v);
+        const bool core = in[u] && hy >= r && hy < r + IN_TS && hx >= r && hx < r + IN_TS;
+        if (core) {
+          const int ci = (hy - r) * IN_TS + (hx - r);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (c < C) bad |= !isfinite(f[u][c]);
+            fs[ci * 4 + c] = T(f[u][c]);               // exact: the values were T
+            ps[ci * 4 + c] = T(pv[u][c]);
+          }
+        }
+      }
+      if (lane < 2 && hb + lane < WH)
+        rowbits[hb + lane] = (unsigned long long)(lane ? bits[2] : bits[0]) |
+                             ((unsigned long long)(lane ? bits[3] : bits[1]) << 32);
+    }
+    if (bad) atomicOr(p.err, 1);
+    __syncthreads();
+    // 2. horizontal dilation: core column cx covers halo columns [cx, cx + 2r]
+    if (tid < WH) {
+      const unsigned long long w = rowbits[tid];
+      unsigned long long d = 0;
+      for (int k = 0; k <= 2 * r; ++k) d |= w >> k;
+      hdil[tid] = (uint32_t)d;
+    }
+    __syncthreads();
+    // 3. vertical dilation: core row cy covers halo rows [cy, cy + 2r]
+    if (tid < IN_TS) {
+      uint32_t m = 0;
+      for (int k = 0; k <= 2 * r; ++k) m |= hdil[tid + k];
+      cmask[tid] = m;
+    }
+    __syncthreads();
+    // 4. emit (writes only)
+#pragma unroll
+    for (int j = 0; j < IN_TS * IN_TS / 256; ++j) {
+      const int i = tid + 256 * j;
+      const int cy = i >> 5, cx = i & 31;
+      const int y = ty * IN_TS + cy, x = tx * IN_TS + cx;
+      if (y >= p.H || x >= p.W) continue;
+      const bool v = (cmask[cy] >> cx) & 1u;
+      const long long pix = sbase + (long long)y * p.W + x;
+      p.mask[pix] = v ? 1 : 0;
+      if (v) ++nact;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c >= C) break;
+        const float f = ld(&fs[i * 4 + c]), pp = ld(&ps[i * 4 + c]);
+        if (v) st(D + pix * p.Cp + c, first ? f : f - pp);
+        st(Pw + pix * C + c, v ? f : pp);          // every pixel of the written buffer
       }
     }
     __syncthreads();
@@ -104,6 +233,11 @@ __global__ void __launch_bounds__(256) k_input(InputParams p) {
 void launch_input(const InputParams& p, int dtype, cudaStream_t st) {
   const int tiles = p.S * ((p.H + IN_TS - 1) / IN_TS) * ((p.W + IN_TS - 1) / IN_TS);
   const int grid = tiles < INPUT_MAX_GRID ? tiles : INPUT_MAX_GRID;
+  if (p.C <= 4 && p.radius >= 1 && p.radius <= IN_RMAX && p.P1 && !getenv("DCNN_INPUT_GENERIC")) {
+    if (dtype == 1) launch_k(k_input_c4<__half>, dim3(grid), dim3(256), 0, st, 1, p);
+    else launch_k(k_input_c4<float>, dim3(grid), dim3(256), 0, st, 1, p);
+    return;
+  }
   if (dtype == 1) launch_k(k_input<__half>, dim3(grid), dim3(256), 0, st, 1, p);
   else launch_k(k_input<float>, dim3(grid), dim3(256), 0, st, 1, p);
 }

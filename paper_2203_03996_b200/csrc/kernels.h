@@ -17,7 +17,12 @@ struct InputParams {
   int Cp;                       // channel pitch of the delta buffer (>= C; pad channels stay 0)
   int radius;                   // Chebyshev dilation radius
   const void* frame;            // [S,H,W,C] T  (F, already in storage dtype)
-  void* P;                      // [S,H,W,C] T  previous propagated input
+  void* P;                      // [S,H,W,C] T  previous propagated input (buffer 0)
+  // radius > 0: P is double-buffered per stream (a CTA's halo reads its neighbours' P, which
+  // they update in the same grid): frame_idx[s] even reads P and writes P1, odd the reverse,
+  // and every pixel of the written buffer is stored.  nullptr: P is updated in place (r = 0).
+  void* P1;
+  const long long* frame_idx;   // [S] advanced once per frame by the bookkeeping kernel
   void* delta;                  // [S,H,W,C] T
   uint8_t* mask;                // [S,H,W]
   const float* eps;             // device slot of eps_in

@@ -179,3 +179,44 @@ def test_host_entry_point_matches_device():
         hb = b.process_frame_host(frames[t])
         torch.cuda.synchronize()
         np.testing.assert_array_equal(out[0].cpu().numpy(), hb[0])
+
+
+@pytest.mark.parametrize("C,r,dt,eps", [(3, 7, "f16", 0.0), (3, 7, "f32", 0.05), (1, 1, "f16", 0.0),
+                                        (4, 16, "f32", 0.0), (2, 3, "f16", -1.0), (8, 2, "f16", 0.0),
+                                        (3, 0, "f16", 0.0)])
+def test_input_stage_masks_and_deltas(C, r, dt, eps):
+    """a1: input mask (threshold + Chebyshev dilation), delta and the
+    propagated input P, bit-exact against the oracle on ragged multi-tile frames (two streams,
+    first frame, moving blobs, eps < 0 = every pixel active)."""
+    from paper_2203_03996_b200 import BUF_MASK, BUF_DELTA
+    H, W = 75, 101                                   # 3 x 4 input tiles, ragged in both axes
+    b = nets._Builder("inp", H, W, C, 0, dt)
+    i = b.conv(-1, 8, 1, act="none")
+    b.net.outputs = [i]
+    b.net.input_eps = eps
+    b.net.input_dilation = r
+    b.net.set_inner_eps(0.0)
+    npdt = np.float16 if dt == "f16" else np.float32
+    c3 = min(C, 3)                                   # the video generator draws <= 3 channels
+    frames = clip([VideoSpec(H, W, C=c3, n_blobs=2, blob_h=9, blob_w=13, speed=4, seed=5, noise_p=0.01),
+                   VideoSpec(H, W, C=c3, n_blobs=1, blob_h=20, blob_w=7, speed=3, seed=6)], 5, dtype=np.float32)
+    while frames.shape[-1] < C:                      # extra channels: reversed, halved copies
+        frames = np.concatenate([frames, 0.5 * frames[..., ::-1][..., :C - frames.shape[-1]]], axis=-1)
+    frames = frames.astype(npdt)
+    eng = _engine(b.net, 2)
+    orc = DeltaOracle(b.net, 2)
+    out = [torch.empty((2,) + s, device="cuda") for s in eng.out_shapes]
+    for t in range(frames.shape[0]):
+        eng.process_frame(torch.from_numpy(np.ascontiguousarray(frames[t])).cuda(), out)
+        torch.cuda.synchronize()
+        orc.step(frames[t])
+        gm = eng.debug_read(-1, BUF_MASK).astype(bool)
+        om = orc.masks[-1]
+        bad = np.argwhere(gm != om)
+        assert len(bad) == 0, (f"frame {t}: {len(bad)} input mask mismatches, first at {bad[:4].tolist()} "
+                               f"gpu {gm[tuple(bad[0])]}")
+        gd = eng.debug_read(-1, BUF_DELTA)[..., :C].astype(np.float64)
+        od = np.asarray(orc.deltas[-1], dtype=np.float64)
+        np.testing.assert_array_equal(np.where(om[..., None], gd, 0.0), np.where(om[..., None], od, 0.0),
+                                      err_msg=f"frame {t}: input delta")
+    eng.close()
