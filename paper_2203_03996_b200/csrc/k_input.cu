@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) k_input(InputParams p) {
 //    word per halo row;
 //  * the dilation is bitwise: OR of 2r+1 shifted row words, then OR of 2r+1 row words;
 //  * the core pixels' F and P stay in shared memory, so the emit pass only writes.
-template <typename T>
+template <typename T, int C>
 __global__ void __launch_bounds__(256, 3) k_input_c4(InputParams p) {
   pdl_trigger();
   pdl_wait();
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(256, 3) k_input_c4(InputParams p) {
   const int WH = IN_TS + 2 * r;
   const T* F = reinterpret_cast<const T*>(p.frame);
   T* D = reinterpret_cast<T*>(p.delta);
-  const int C = p.C;
+  // C: compile-time channel count (1..4)
   const float eps = *p.eps;
   unsigned nact = 0;
   for (int b = blockIdx.x; b < p.S * tiles_y * tiles_x; b += gridDim.x) {
@@ -143,6 +143,8 @@ __global__ void __launch_bounds__(256, 3) k_input_c4(InputParams p) {
     const bool all = first || eps < 0.f;
     const int y0 = ty * IN_TS - r, x0 = tx * IN_TS - r;
     const long long sbase = (long long)s * p.H * p.W;
+    const T* Fs = F + sbase * C;                   // this stream's frame: 32-bit offsets below
+    const T* Ps = P + sbase * C;
     bool bad = false;
     // 1. threshold: warp w takes halo rows 2w, 2w+1, 2w+16, 2w+17, ...
     for (int hb = 2 * warp; hb < WH; hb += 16) {
@@ -155,13 +157,16 @@ __global__ void __launch_bounds__(256, 3) k_input_c4(InputParams p) {
         in[u] = hy < WH && hx < WH && y >= 0 && y < p.H && x >= 0 && x < p.W;
         // unconditional loads from a clamped in-bounds address, then a select: no branch per load
         const int yc = min(max(y, 0), p.H - 1), xc = min(max(x, 0), p.W - 1);
-        const long long base = (sbase + (long long)yc * p.W + xc) * C;
+        const int o = (yc * p.W + xc) * C;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const long long o = base + min(c, C - 1);
-          const float fr = ld(F + o), pr = ld(P + o);
-          f[u][c] = (in[u] && c < C) ? fr : 0.f;
-          pv[u][c] = (in[u] && c < C && !first) ? pr : 0.f;
+          if (c < C) {
+            const float fr = ld(Fs + o + c), pr = ld(Ps + o + c);
+            f[u][c] = in[u] ? fr : 0.f;
+            pv[u][c] = (in[u] && !first) ? pr : 0.f;
+          } else {
+            f[u][c] = pv[u][c] = 0.f;
+          }
         }
       }
       uint32_t bits[4];
@@ -233,9 +238,16 @@ __global__ void __launch_bounds__(256, 3) k_input_c4(InputParams p) {
 void launch_input(const InputParams& p, int dtype, cudaStream_t st) {
   const int tiles = p.S * ((p.H + IN_TS - 1) / IN_TS) * ((p.W + IN_TS - 1) / IN_TS);
   const int grid = tiles < INPUT_MAX_GRID ? tiles : INPUT_MAX_GRID;
-  if (p.C <= 4 && p.radius >= 1 && p.radius <= IN_RMAX && p.P1 && !getenv("DCNN_INPUT_GENERIC")) {
-    if (dtype == 1) launch_k(k_input_c4<__half>, dim3(grid), dim3(256), 0, st, 1, p);
-    else launch_k(k_input_c4<float>, dim3(grid), dim3(256), 0, st, 1, p);
+  if (p.C <= 4 && p.radius >= 1 && p.radius <= IN_RMAX && p.P1 && (long long)p.H * p.W * p.C < (1ll << 31) &&
+      !getenv("DCNN_INPUT_GENERIC")) {
+    auto go = [&](auto kern) { launch_k(kern, dim3(grid), dim3(256), 0, st, 1, p); };
+    if (dtype == 1) {
+      if (p.C == 1) go(k_input_c4<__half, 1>); else if (p.C == 2) go(k_input_c4<__half, 2>);
+      else if (p.C == 3) go(k_input_c4<__half, 3>); else go(k_input_c4<__half, 4>);
+    } else {
+      if (p.C == 1) go(k_input_c4<float, 1>); else if (p.C == 2) go(k_input_c4<float, 2>);
+      else if (p.C == 3) go(k_input_c4<float, 3>); else go(k_input_c4<float, 4>);
+    }
     return;
   }
   if (dtype == 1) launch_k(k_input<__half>, dim3(grid), dim3(256), 0, st, 1, p);
