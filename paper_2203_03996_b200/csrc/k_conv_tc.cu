@@ -117,6 +117,25 @@ __device__ __forceinline__ float2 unpack_h2(uint32_t u) {
 }
 
 // raw 16-B loads of cache rows (kept packed in registers until the accumulator lands)
+// Activation in the tensor-core epilogue (fp16 nets only).  SiLU / sigmoid through
+// sigmoid(x) = 0.5 + 0.5 tanh(x / 2): one MUFU op (tanh.approx) instead of two (ex2 + rcp).
+// The wide truncating epilogues evaluate f four times per element (f(x^A) and f(s) in both
+// passes) and were MUFU-throughput bound.  The approximation error (~2^-11 relative) is at the
+// fp16 storage precision of the deltas and caches; f stays deterministic, so s == x^A still
+// gives an exactly-zero delta (the product is rounded, never contracted).
+template <int ACT>
+__device__ __forceinline__ float act_tc(float x, float param) {
+  if constexpr (ACT == ACT_SILU || ACT == ACT_SIGMOID) {
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+    const float sg = fmaf(0.5f, t, 0.5f);
+    if constexpr (ACT == ACT_SILU) return __fmul_rn(x, sg);
+    else return sg;
+  } else {
+    return act_t<ACT>(x, param);
+  }
+}
+
 template <typename TC>
 __device__ __forceinline__ void unpack8(const uint4& u, float v[8]);
 template <>
@@ -698,9 +717,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             float o[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-              const float prev = first ? 0.f : act_t<ACT>(a[k], e.act_param);
+              const float prev = first ? 0.f : act_tc<ACT>(a[k], e.act_param);
               const float sv = a[k] + t[k] + z[k];
-              const float d = act_t<ACT>(sv, e.act_param) - prev;
+              const float d = act_tc<ACT>(sv, e.act_param) - prev;
               if (c0 + k < C) mx = fmaxf(mx, fabsf(d));
               o[k] = d;
               a[k] = sv;                       // x^A if updated (Eq. 6)
@@ -752,9 +771,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             if (trunc) {
-              const float prev = first ? 0.f : act_t<ACT>(a[k], e.act_param);
+              const float prev = first ? 0.f : act_tc<ACT>(a[k], e.act_param);
               const float sv = a[k] + t[k] + z[k];
-              o[k] = rnd<__half>(act_t<ACT>(sv, e.act_param) - prev);
+              o[k] = rnd<__half>(act_tc<ACT>(sv, e.act_param) - prev);
               if (upd) { a[k] = sv; t[k] = 0.f; }                 // Eq. 6: x^A := s
               else t[k] += z[k];                                   // x^T += dx
             } else {
