@@ -160,8 +160,10 @@ DCNN_API dcnn_status dcnn_process_frame_host(dcnn_net* net, const void* host_fra
                                     void* const* host_outputs, void* stream);
 
 /* Flush the caches of one stream (or all with -1): its next frame is dense
- * again (PAPER.md:715-719 S1.4).  Ordered after work previously enqueued by
- * process_frame on this net. */
+ * again (PAPER.md:715-719 S1.4).  No device work is enqueued here: the request is
+ * recorded on the host and applied on the stream of the NEXT process_frame call,
+ * so it is ordered after every frame enqueued before it and before that frame,
+ * whichever stream the caller uses. */
 DCNN_API dcnn_status dcnn_reset(dcnn_net* net, int32_t stream);
 
 DCNN_API void dcnn_destroy_net(dcnn_net* net);

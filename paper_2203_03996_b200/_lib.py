@@ -170,24 +170,47 @@ class DeltaNet:
         """frames: torch CUDA tensor [S,H,W,C] in the net dtype; outputs: list of fp32 CUDA
         tensors (or None).  Enqueued on ``stream`` (torch stream, default: current)."""
         import torch
+        want_dt = torch.float16 if self.dtype == "f16" else torch.float32
+        fshape = (self.S, self.net.in_h, self.net.in_w, self.net.in_c)
+        if not frames.is_cuda or frames.dtype != want_dt or tuple(frames.shape) != fshape \
+                or not frames.is_contiguous():
+            raise ValueError(f"frames must be a contiguous CUDA {want_dt} tensor of shape {fshape}, got "
+                             f"{frames.dtype} {tuple(frames.shape)} on {frames.device}")
         if stream is None:
             stream = torch.cuda.current_stream(frames.device)
         optr = None
         if outputs is not None:
+            self._check_outputs(outputs, lambda o: (o.is_cuda and o.dtype == torch.float32 and o.is_contiguous()
+                                                    and o.device == frames.device, tuple(o.shape)))
             optr = (C.c_void_p * len(outputs))(*[o.data_ptr() for o in outputs])
         _check(self.lib, self.lib.dcnn_process_frame(self.h, C.c_void_p(frames.data_ptr()), optr,
                                                      C.c_void_p(stream.cuda_stream)))
 
     def process_frame_host(self, frames: np.ndarray, outputs=None, stream=None):
         """Host numpy frames in, host numpy fp32 outputs out (synchronous)."""
-        fr = np.ascontiguousarray(frames)
+        fshape = (self.S, self.net.in_h, self.net.in_w, self.net.in_c)
+        fr = np.ascontiguousarray(frames, dtype=np.float16 if self.dtype == "f16" else np.float32)
+        if fr.shape != fshape:
+            raise ValueError(f"frames must have shape {fshape}, got {fr.shape}")
         if outputs is None:
             outputs = [np.empty((self.S,) + s, np.float32) for s in self.out_shapes]
+        self._check_outputs(outputs, lambda o: (isinstance(o, np.ndarray) and o.dtype == np.float32
+                                                and o.flags.c_contiguous, o.shape))
         optr = (C.c_void_p * len(outputs))(*[o.ctypes.data for o in outputs])
         sp = 0 if stream is None else stream.cuda_stream
         _check(self.lib, self.lib.dcnn_process_frame_host(self.h, C.c_void_p(fr.ctypes.data), optr,
                                                           C.c_void_p(sp)))
         return outputs
+
+    def _check_outputs(self, outputs, props):
+        """One fp32 contiguous buffer of S*Ho*Wo*Co elements per output op (the library writes
+        exactly that many floats through each pointer)."""
+        if len(outputs) != len(self.out_shapes):
+            raise ValueError(f"expected {len(self.out_shapes)} output buffers, got {len(outputs)}")
+        for k, (o, shp) in enumerate(zip(outputs, self.out_shapes)):
+            ok, got = props(o)
+            if not ok or int(np.prod(got)) != self.S * int(np.prod(shp)):
+                raise ValueError(f"output {k} must be a contiguous fp32 buffer of shape {(self.S,) + shp}, got {got}")
 
     def reset(self, stream: int = -1):
         _check(self.lib, self.lib.dcnn_reset(self.h, stream))

@@ -87,6 +87,26 @@ __device__ __forceinline__ float act_t(float x, float param) {
   else return x;
 }
 
+// Activation of the fp16 nets (delta storage type T = __half), shared by EVERY fp16 epilogue
+// (tcgen05 conv, CUDA-core conv, add/act kernels) so that a pixel whose tiles move between
+// kernels (hybrid dispatch) always sees the same f: SiLU / sigmoid through
+// sigmoid(x) = 0.5 + 0.5 tanh(x / 2), one MUFU op (tanh.approx) instead of two (ex2 + rcp).
+// The approximation error (~2^-11 relative) is at the fp16 storage precision of the deltas
+// and caches; f stays deterministic and its product rounded, so s == x^A still gives an
+// exactly-zero delta.  fp32 nets (T = float) keep act_t.
+template <typename T, int ACT>
+__device__ __forceinline__ float act_n(float x, float param) {
+  if constexpr (std::is_same<T, __half>::value && (ACT == ACT_SILU || ACT == ACT_SIGMOID)) {
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+    const float sg = fmaf(0.5f, t, 0.5f);
+    if constexpr (ACT == ACT_SILU) return __fmul_rn(x, sg);
+    else return sg;
+  } else {
+    return act_t<ACT>(x, param);
+  }
+}
+
 // host-side: call f(std::integral_constant<int, ACT>) for the runtime activation code
 template <typename F>
 inline void act_dispatch(int act, F&& f) {
@@ -170,8 +190,8 @@ __device__ __forceinline__ bool warp_finish_pixel(const Epi& e, long long pix, i
         const float a = first ? 0.f : ld(A + c);
         const float t = first ? 0.f : ld(Tt + c);
         const float sum = a + t + z;                         // x^A + x^T + dx
-        const float prev = first ? 0.f : act_t<ACT>(a, e.act_param);
-        const float d = act_t<ACT>(sum, e.act_param) - prev;   // Eq. 5
+        const float prev = first ? 0.f : act_n<T, ACT>(a, e.act_param);
+        const float d = act_n<T, ACT>(sum, e.act_param) - prev;   // Eq. 5
         zv[k] = z; tv[k] = t; sv[k] = sum; dv[k] = d;
         mx = fmaxf(mx, fabsf(d));
       }
@@ -238,8 +258,8 @@ __device__ __forceinline__ bool group_finish_pixel(const Epi& e, long long pix, 
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const float prev = first ? 0.f : act_t<ACT>(a[q][k], e.act_param);
-          const float d = act_t<ACT>(a[q][k] + t[q][k] + z[q][k], e.act_param) - prev;   // Eq. 5
+          const float prev = first ? 0.f : act_n<T, ACT>(a[q][k], e.act_param);
+          const float d = act_n<T, ACT>(a[q][k] + t[q][k] + z[q][k], e.act_param) - prev;   // Eq. 5
           mx = fmaxf(mx, fabsf(d));
         }
       }
@@ -256,8 +276,8 @@ __device__ __forceinline__ bool group_finish_pixel(const Epi& e, long long pix, 
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             sv[k] = a[q][k] + t[q][k] + z[q][k];
-            const float prev = first ? 0.f : act_t<ACT>(a[q][k], e.act_param);
-            dv[k] = rnd<T>(act_t<ACT>(sv[k], e.act_param) - prev);
+            const float prev = first ? 0.f : act_n<T, ACT>(a[q][k], e.act_param);
+            dv[k] = rnd<T>(act_n<T, ACT>(sv[k], e.act_param) - prev);
           }
           st8(A + 8 * j, sv);                                // Eq. 6
           st8_zero(Tt + 8 * j);

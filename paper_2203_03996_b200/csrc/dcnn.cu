@@ -117,6 +117,7 @@ struct dcnn_net {
   cudaGraphExec_t exec = nullptr;
   int kernels = 0;
   cudaStream_t last = nullptr;
+  std::vector<uint8_t> reset_req;   // [S] dcnn_reset requests, applied on the next frame's stream
   // host staging for the _host entry point
   void* h_frames = nullptr;
   size_t frame_bytes = 0;
@@ -921,10 +922,24 @@ dcnn_status dcnn_set_threshold(dcnn_net* n, int32_t op, float eps) {
 dcnn_status dcnn_reset(dcnn_net* n, int32_t stream) {
   if (!n) return fail(DCNN_ERR_ARG, "null net");
   if (stream < -1 || stream >= n->S) return fail(DCNN_ERR_ARG, "stream index");
-  CUDA_TRY(cudaSetDevice(n->device));
-  cudaStream_t st = n->last ? n->last : n->cap;
-  if (stream < 0) CUDA_TRY(cudaMemsetAsync(n->pend, 1, n->S, st));
-  else CUDA_TRY(cudaMemsetAsync(n->pend + stream, 1, 1, st));
+  // recorded on the host and applied on the stream of the next process_frame (whatever
+  // stream that is), so the reset is ordered after every earlier frame and before the next
+  if ((int)n->reset_req.size() != n->S) n->reset_req.assign(n->S, 0);
+  for (int s = 0; s < n->S; ++s)
+    if (stream < 0 || s == stream) n->reset_req[s] = 1;
+  return DCNN_OK;
+}
+
+// pending dcnn_reset requests -> pend[s] := 1, enqueued on the frame's stream
+static dcnn_status apply_resets(dcnn_net* n, cudaStream_t st) {
+  for (int s = 0; s < (int)n->reset_req.size(); ++s) {
+    if (!n->reset_req[s]) continue;
+    int e = s;
+    while (e + 1 < (int)n->reset_req.size() && n->reset_req[e + 1]) ++e;
+    CUDA_TRY(cudaMemsetAsync(n->pend + s, 1, (size_t)(e - s + 1), st));
+    for (int k = s; k <= e; ++k) n->reset_req[k] = 0;
+    s = e;
+  }
   return DCNN_OK;
 }
 
@@ -940,6 +955,7 @@ dcnn_status dcnn_process_frame(dcnn_net* n, const void* frames, void* const* out
   if (s) return s;
   if ((s = build_graph(n))) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((s = apply_resets(n, st))) return s;
   if (n->timing_mask) {
     // profiling graph (no per-call nodes): stage the frame and copy outputs around it
     CUDA_TRY(cudaMemcpyAsync(n->frame_in, frames, n->frame_bytes, cudaMemcpyDeviceToDevice, st));
@@ -967,6 +983,7 @@ dcnn_status dcnn_process_frame_host(dcnn_net* n, const void* host_frames, void* 
   if (s) return s;
   if ((s = build_graph(n))) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((s = apply_resets(n, st))) return s;
   CUDA_TRY(cudaMemcpyAsync(n->frame_in, host_frames, n->frame_bytes, cudaMemcpyHostToDevice, st));
   if (!n->timing_mask && (s = set_frame_io(n, n->frame_in, nullptr))) return s;
   CUDA_TRY(cudaGraphLaunch(n->exec, st));

@@ -116,24 +116,10 @@ __device__ __forceinline__ float2 unpack_h2(uint32_t u) {
   return make_float2(__half2float(__ushort_as_half(lo)), __half2float(__ushort_as_half(hi)));
 }
 
-// raw 16-B loads of cache rows (kept packed in registers until the accumulator lands)
-// Activation in the tensor-core epilogue (fp16 nets only).  SiLU / sigmoid through
-// sigmoid(x) = 0.5 + 0.5 tanh(x / 2): one MUFU op (tanh.approx) instead of two (ex2 + rcp).
-// The wide truncating epilogues evaluate f four times per element (f(x^A) and f(s) in both
-// passes) and were MUFU-throughput bound.  The approximation error (~2^-11 relative) is at the
-// fp16 storage precision of the deltas and caches; f stays deterministic, so s == x^A still
-// gives an exactly-zero delta (the product is rounded, never contracted).
+// Activation: act_n<__half, ACT> (common.cuh), the one f of every fp16 epilogue.
 template <int ACT>
 __device__ __forceinline__ float act_tc(float x, float param) {
-  if constexpr (ACT == ACT_SILU || ACT == ACT_SIGMOID) {
-    float t;
-    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
-    const float sg = fmaf(0.5f, t, 0.5f);
-    if constexpr (ACT == ACT_SILU) return __fmul_rn(x, sg);
-    else return sg;
-  } else {
-    return act_t<ACT>(x, param);
-  }
+  return act_n<__half, ACT>(x, param);
 }
 
 template <typename TC>

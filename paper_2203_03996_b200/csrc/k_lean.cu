@@ -370,8 +370,8 @@ __global__ void __launch_bounds__(256) k_add_lean(PwParams p, int lg_nch) {
       float mx = 0.f;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const float prev = first ? 0.f : act_t<ACT>(a[c], e.act_param);
-        d[c] = act_t<ACT>(a[c] + t[c] + z[c], e.act_param) - prev;   // Eq. 5
+        const float prev = first ? 0.f : act_n<__half, ACT>(a[c], e.act_param);
+        d[c] = act_n<__half, ACT>(a[c] + t[c] + z[c], e.act_param) - prev;   // Eq. 5
         mx = fmaxf(mx, fabsf(d[c]));
       }
       for (int o = nch >> 1; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
