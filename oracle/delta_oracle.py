@@ -219,6 +219,9 @@ class DeltaOracle:
         self.deltas = {}     # op index -> fp64 delta (valid on its mask)
         self.conv_masks = {}  # conv op -> pre-truncation output mask (receptive-field OR)
         self.frame_index = np.zeros(n_streams, dtype=np.int64)
+        # decision-forced replay (reading R-replay)
+        self._force = None
+        self.replay = {"adopted": 0, "hard": 0, "hard_ops": [], "decisions": 0}
 
     # PAPER.md:715-719 (S1.4): "reset the buffers ... to flush all accumulated errors"
     def reset(self, stream=-1):
@@ -254,6 +257,8 @@ class DeltaOracle:
         d = act_fn(f, s) - prev                                 # Eq. 5
         dmax = np.max(np.abs(d), axis=-1)
         upd = m_in & (fb | (eps < 0) | (dmax > eps))            # Z1 strict, Z22
+        if self._force is not None and i in self._force:
+            upd = self._forced_decision(i, upd, dmax, eps, s, A_eff, m_in & ~fb & (eps >= 0))
         trn = m_in & ~upd
         # updated pixels: x^A := x^A + x^T + dx (Eq. 6), x^T := 0
         self.A[i] = np.where(upd[..., None], self._qc(s), np.where(fb[..., None], 0.0, A))
@@ -262,8 +267,38 @@ class DeltaOracle:
         dout = np.where(upd[..., None], self._q(d), 0.0)
         return dout, upd
 
-    def step(self, frames):
-        """Advance every stream by one frame; returns the dense outputs O^i (fp64)."""
+    # relative width of the rounding band of a truncation decision, per storage dtype: the
+    # decision "max_c|d| > eps" of a pipeline that stores in fp16 (fp32) can legitimately differ
+    # from this fp64 one only where max_c|d| lies within the storage rounding of the values it
+    # is formed from (4e-3 relative for fp16, 1e-5 for fp32)
+    BAND = {"f16": 4e-3, "f32": 1e-5, "f64": 0.0}
+
+    def _forced_decision(self, i, upd, dmax, eps, s, A, decided):
+        """Decision-forced replay (TEST USE ONLY).  Where this oracle's own decision lies within
+        the rounding band of eps, |max_c|d| - eps| <= BAND * max(1, max_c|x^A + x^T + dx|,
+        max_c|x^A|), both outcomes are correct results of the method in finite precision and
+        the decision given in ``force[i]`` (the other pipeline's) is adopted, so that both
+        continue from the same state.  Outside the band the oracle's own decision stands and a
+        differing ``force[i]`` is counted as a hard disagreement (a failure for the caller)."""
+        other = np.asarray(self._force[i], dtype=bool)
+        scale = np.maximum(1.0, np.maximum(np.max(np.abs(s), axis=-1), np.max(np.abs(A), axis=-1)))
+        band = self.BAND[self.dt if self.dt in self.BAND else "f64"] * scale
+        near = decided & (np.abs(dmax - eps) <= band)
+        differ = decided & (other != upd)
+        self.replay["decisions"] += int(decided.sum())
+        self.replay["adopted"] += int((near & differ).sum())
+        hard = int((differ & ~near).sum())
+        if hard:
+            self.replay["hard"] += hard
+            self.replay["hard_ops"].append((i, hard))
+        return np.where(near, other & decided, upd)
+
+    def step(self, frames, force=None):
+        """Advance every stream by one frame; returns the dense outputs O^i (fp64).
+
+        ``force`` (tests only): {op index: bool [S,H,W] output mask of another pipeline} for
+        decision-forced replay of the truncation decisions (see _forced_decision)."""
+        self._force = force
         net, S = self.net, self.S
         F = np.asarray(frames, dtype=np.float64)      # already in the storage dtype
         assert F.shape[0] == S

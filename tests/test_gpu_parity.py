@@ -7,7 +7,7 @@ import pytest
 from oracle import DeltaOracle
 from synth import nets
 from synth.frames import VideoSpec, cfg1_frames, clip
-from helpers import max_abs_rel
+from helpers import max_abs_rel, lockstep
 
 pytestmark = pytest.mark.gpu
 
@@ -84,18 +84,20 @@ def test_cfg2_integer_exact():
 
 @pytest.mark.parametrize("dtype,tol", [("f32", 1e-4), ("f16", 2e-2)])
 def test_cfg2_toy_eps005(dtype, tol):
-    """BASELINE configs[1]: toy 128x128x64, eps = 0.05, ~10 % changed pixels, 30 frames."""
+    """BASELINE configs[1]: toy 128x128x64, eps = 0.05, ~10 % changed pixels, 30 frames; masks
+    equal after decision-forced replay."""
     net = nets.toy_net(dtype=dtype)
     dt = np.float16 if dtype == "f16" else np.float32
     frames = clip([VideoSpec(128, 128, n_blobs=3, blob_h=22, blob_w=22, speed=3, noise_p=0.01,
                              seed=2)], 30, dt)
-    worst, agree, _ = run_both(net, frames, check_masks="agree", tol=tol)
-    print(f"cfg2 {dtype}: worst max-abs-rel {worst:.2e}, min mask agreement {agree:.6f}")
+    rec, _ = lockstep(net, frames, tol=tol, masks="replay", name=f"cfg2_toy_{dtype}_eps005")
+    print(rec)
 
 
 @pytest.mark.parametrize("seed", range(10))
 def test_random_graphs_eps0(seed):
-    """SPEC S:424 zero-threshold equivalence on random graphs, GPU vs oracle, fp32."""
+    """SPEC S:424 zero-threshold equivalence on random graphs, GPU vs oracle, fp32: masks of
+    every layer bit-exact (north_star, threshold 0), outputs within 1e-4."""
     net = nets.random_net(seed, n_layers=4 + seed % 7, dtype="f32", eps=0.0)
     rng = np.random.default_rng(seed)
     S = 2
@@ -105,7 +107,7 @@ def test_random_graphs_eps0(seed):
         ch = rng.random((S, net.in_h, net.in_w)) < 0.1
         x = np.where(ch[..., None], rng.standard_normal(x.shape), x).astype(np.float32)
         frames.append(x)
-    run_both(net, np.stack(frames), check_masks="agree", mask_agree=0.999, tol=1e-4)
+    lockstep(net, np.stack(frames), tol=1e-4, masks="exact", name=f"random_dag_{seed}_eps0")
 
 
 def test_static_clip_empty_masks_and_constant_output():

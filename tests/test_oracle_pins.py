@@ -399,3 +399,143 @@ def test_net_tables_match_published_sizes():
     for L in yo.layers:
         ops[L.op] = ops.get(L.op, 0) + 1
     assert ops == {"conv": 60, "add": 7, "concat": 13, "maxpool": 3, "up": 2}
+
+
+# ----------------------------------------------------------------------------- Z12 storage
+def _num(v):
+    return float(v) if not isinstance(v, str) else float(v)
+
+
+@pytest.mark.parametrize("dtype,key", [("f16", "fp16_rne"), ("f32", "fp32_rne")])
+def test_quantize_round_to_nearest_even(dtype, key):
+    """quantize() against hand values of IEEE 754 RNE (ties to even, overflow to inf,
+    subnormals): an fp16 branch that rounded to fp32 (or truncated) fails here."""
+    from oracle import quantize
+    for x, want in GOLD[key]["cases"]:
+        got = quantize(np.array([x]), dtype)[0]
+        assert got == _num(want), (dtype, x, got, want)
+
+
+@pytest.mark.parametrize("cache", ["f16", "f32"])
+def test_fp16_storage_rounding_placement(cache):
+    """Z12: where the oracle rounds (weights, emitted delta, caches) against a hand derivation
+    in binary16 (tests/golden/fixtures.json fp16_storage_placement)."""
+    g = GOLD["fp16_storage_placement"]
+    b = nets._Builder("q", 1, 1, 1, 0, "f16")
+    i = b.conv(-1, 1, 1, act="relu")
+    L = b.net.layers[i]
+    L.weight[...] = g["w"]
+    L.bias[...] = 0.0
+    L.eps = 0.0
+    b.net.outputs = [i]
+    b.net.input_eps = 0.0
+    b.net.cache_dtype = cache
+    o = DeltaOracle(b.net, 1)
+    for t, x in enumerate(g["x"]):
+        out = o.step(np.full((1, 1, 1, 1), x))[0][0, 0, 0, 0]
+        assert o.deltas[i][0, 0, 0, 0] == g["delta"][t]
+        assert out == g["O"][t]
+        assert o.A[i][0, 0, 0, 0] == g[f"xA_{cache}_cache"][t]
+
+
+def test_concat_channel_order():
+    """Z10: concat([x, 2x]) emits [dx, 2dx] and concat([2x, x]) emits [2dx, dx] (operand order
+    is the channel order; torch.cat semantics)."""
+    b = nets._Builder("cat", 3, 3, 2, 0, "f64")
+    two = b.add([-1, -1])                               # 2x
+    c1 = b.concat([-1, two])
+    c2 = b.concat([two, -1])
+    b.net.outputs = [c1, c2]
+    b.net.input_eps = 0.0
+    o = DeltaOracle(b.net, 1, storage="f64")
+    o.step(np.zeros((1, 3, 3, 2)))
+    x = np.zeros((1, 3, 3, 2))
+    x[0, 1, 1] = [1.0, -3.0]
+    o.step(x)
+    assert (o.deltas[c1][0, 1, 1] == [1.0, -3.0, 2.0, -6.0]).all()
+    assert (o.deltas[c2][0, 1, 1] == [2.0, -6.0, 1.0, -3.0]).all()
+    ref = torch.cat([torch.tensor(x), 2 * torch.tensor(x)], -1).numpy()
+    np.testing.assert_array_equal(o.O[c1], ref)
+
+
+# ----------------------------------------------------------------------------- c5.2(ii)
+def test_forced_replay_self_consistent_and_hard_failures():
+    """Decision-forced replay: forcing the oracle's own decisions changes nothing; forcing the
+    opposite of decisions far from eps is counted as hard disagreement and NOT adopted."""
+    net = nets.toy_net(32, 32, 8, eps=0.05, dtype="f16")
+    fr = clip([VideoSpec(32, 32, n_blobs=2, blob_h=6, blob_w=6, speed=2, seed=4)], 4, np.float16)
+    a = DeltaOracle(net, 1)
+    b = DeltaOracle(net, 1)
+    c = DeltaOracle(net, 1)
+    trunc = [i for i, L in enumerate(net.layers) if L.truncates]
+    for t in range(4):
+        oa = a.step(fr[t])
+        ob = b.step(fr[t], force={i: a.masks[i] for i in trunc})
+        oc = c.step(fr[t], force={i: ~a.masks[i] for i in trunc})
+        np.testing.assert_array_equal(oa[0], ob[0])
+        np.testing.assert_array_equal(oa[0], oc[0])     # far-from-eps decisions are kept
+    assert b.replay["adopted"] == 0 and b.replay["hard"] == 0 and b.replay["decisions"] > 0
+    assert c.replay["hard"] > 0 and c.replay["adopted"] <= c.replay["decisions"]
+
+
+def test_forced_replay_adopts_decision_at_the_threshold():
+    """A pixel whose max-norm equals eps exactly (truncated under the strict rule Z1) is inside
+    every band: the other pipeline's 'update' is adopted (S:144-style identity ReLU, eps 1.5)."""
+    b = nets._Builder("id", 1, 1, 1, 0, "f16")
+    i = b.conv(-1, 1, 1, act="relu")
+    b.net.layers[i].weight[...] = 1.0
+    b.net.layers[i].bias[...] = 0.0
+    b.net.layers[i].eps = 1.5
+    b.net.outputs = [i]
+    b.net.input_eps = 0.0
+    free, forced = DeltaOracle(b.net, 1), DeltaOracle(b.net, 1)
+    for o in (free, forced):
+        o.step(np.zeros((1, 1, 1, 1)))
+    x = np.full((1, 1, 1, 1), 1.5)
+    assert free.step(x)[0][0, 0, 0, 0] == 0.0                          # 1.5 > 1.5 is false
+    assert forced.step(x, force={i: np.ones((1, 1, 1), bool)})[0][0, 0, 0, 0] == 1.5
+    assert forced.replay["adopted"] == 1 and forced.replay["hard"] == 0
+    assert forced.T[i][0, 0, 0, 0] == 0.0 and forced.A[i][0, 0, 0, 0] == 1.5
+
+
+# ----------------------------------------------------------------------------- dense reference
+def _torch_dense(net, x):
+    """The layer table executed with torch's fp64 library ops (F.conv2d, F.max_pool2d, ...),
+    NCHW: an implementation independent of the oracle's numpy per-tap matmuls."""
+    acts = {"none": lambda t: t, "relu": Fnn.relu, "silu": Fnn.silu, "relu6": Fnn.relu6,
+            "leaky": lambda t: Fnn.leaky_relu(t, 0.1), "sigmoid": torch.sigmoid}
+    vals = {-1: torch.from_numpy(np.asarray(x, np.float64)).permute(0, 3, 1, 2)}
+    for i, L in enumerate(net.layers):
+        xs = [vals[j] for j in L.inputs]
+        if L.op == "conv":
+            w = torch.from_numpy(L.weight.astype(np.float64)).permute(0, 3, 1, 2)
+            y = acts[L.act](Fnn.conv2d(xs[0], w, torch.from_numpy(L.bias.astype(np.float64)), L.stride, L.pad,
+                                       L.dil, L.groups))
+        elif L.op == "act":
+            y = acts[L.act](xs[0])
+        elif L.op == "maxpool":
+            y = Fnn.max_pool2d(xs[0], L.kh, L.stride, L.pad)
+        elif L.op == "avgpool":
+            y = Fnn.avg_pool2d(xs[0], L.kh, L.stride, L.pad, count_include_pad=True)
+        elif L.op == "up":
+            y = Fnn.interpolate(xs[0], scale_factor=L.up, mode="nearest")
+        elif L.op == "add":
+            y = acts[L.act](sum(xs))
+        elif L.op == "concat":
+            y = torch.cat(xs, 1)
+        elif L.op == "affine":
+            y = xs[0] * torch.from_numpy(L.scale.astype(np.float64))[:, None, None] + \
+                torch.from_numpy(L.shift.astype(np.float64))[:, None, None]
+        vals[i] = y
+    return [vals[o].permute(0, 2, 3, 1).numpy() for o in net.outputs]
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_dense_forward_matches_torch_library(seed):
+    """dense_forward (the ε <= 0 result definition) against torch fp64 library ops on random
+    DAGs over every op kind, and on the toy net."""
+    net = nets.random_net(seed, n_layers=5 + seed, dtype="f64", eps=0.0) if seed else nets.toy_net(32, 32, 8)
+    net.dtype = "f64"
+    x = np.random.default_rng(seed).standard_normal((2, net.in_h, net.in_w, net.in_c))
+    for a, b in zip(dense_forward(net, x, wdtype="f64"), _torch_dense(net, x)):
+        np.testing.assert_allclose(a, b, rtol=1e-11, atol=1e-11)
