@@ -110,8 +110,10 @@ class Video:
             x0 = self._reflect(px, vx, t, s.W - bw)
             img[y0:y0 + bh, x0:x0 + bw, :] = tex
         if s.noise_p > 0:
-            yy, xx, cc = np.meshgrid(np.arange(s.H), np.arange(s.W), np.arange(s.C), indexing="ij")
-            r = h(s.seed, 5, t, yy, xx, cc)
+            # broadcast (not meshgrid) index arrays: identical hash values, and only the last
+            # SplitMix64 round runs over all H*W*C elements
+            r = h(s.seed, 5, t, np.arange(s.H)[:, None, None], np.arange(s.W)[None, :, None],
+                  np.arange(s.C)[None, None, :])
             hit = (r % np.uint64(1_000_000)).astype(np.int64) < int(round(s.noise_p * 1_000_000))
             sign = np.where(((r >> np.uint64(40)) & np.uint64(1)) == 1, 1, -1)
             img = img + np.where(hit, sign, 0)
@@ -161,3 +163,24 @@ def cfg1_frames(kind: str, n_frames: int = 8, H: int = 32, W: int = 32, C: int =
         f[y0:y0 + block, x0:x0 + block, :] = draw((block, block, C))
         frames.append(f.astype(np.float32)[None])
     return np.stack(frames)
+
+
+def _stream_frames(args):
+    spec, t0, n_frames, dtype = args
+    v = Video(spec)
+    return np.stack([v.frame(t, dtype) for t in range(t0, t0 + n_frames)])
+
+
+def clip_parallel(specs, n_frames, dtype=np.float32, t0=0, workers=None):
+    """clip() with one worker process per stream (same values; frame generation is the slow part
+    of the full-size benchmarks).  Frames [T, S, H, W, C] for t = t0 .. t0 + n_frames - 1."""
+    import multiprocessing as mproc
+    import os
+    args = [(s, t0, n_frames, dtype) for s in specs]
+    workers = min(len(specs), workers or os.cpu_count() or 1)
+    if workers <= 1 or len(specs) == 1:
+        per = [_stream_frames(a) for a in args]
+    else:
+        with mproc.get_context("fork").Pool(workers) as pool:
+            per = pool.map(_stream_frames, args)
+    return np.stack(per, axis=1)
