@@ -237,7 +237,7 @@ def cpu_oracle_time(net, frames, budget_s=12.0):
     with threadpoolctl.threadpool_limits(nproc):
         t0 = time.perf_counter()
         n = 0
-        while t < fr.shape[0] and (n == 0 or time.perf_counter() - t0 < budget_s):
+        while t < fr.shape[0] - 1 and (n == 0 or time.perf_counter() - t0 < budget_s):
             o.step(fr[t])
             t += 1
             n += 1
@@ -573,7 +573,8 @@ def d9_points(args, r):
       (i)   accuracy budget: largest global tau with deviation <= 3 % of max|output|
       (ii)  paper sparsity: smallest tau with MAC fraction <= 16 % (u_conv ~ 6 %)
       (iii) dense mode: every eps < 0, input included (the paper's 'ours dense')"""
-    t_end = min(r.frames.shape[0], args.warmup + 6)
+    steps_pt = min(args.steps, 15)
+    t_end = min(r.frames.shape[0], args.warmup + steps_pt)   # the window time_point() reports
     dfps, _ = r.dense_fps(args.warmup, min(10, args.steps))
     pts = {}
     lo, _, hi, _ = bisect_tau(r, lambda c: c["deviation_vs_dense"] <= 0.03, t_end)
@@ -582,7 +583,7 @@ def d9_points(args, r):
     tau_ii = hi if hi is not None else lo          # first tau at or below 16 % of the dense MACs
     for name, tau, eps_in in (("accuracy_budget", tau_i, None), ("paper_sparsity", tau_ii, None),
                               ("dense_mode", -1.0, -1.0)):
-        fps, ms, c = time_point(r, args, tau, eps_in, steps=min(args.steps, 15))
+        fps, ms, c = time_point(r, args, tau, eps_in, steps=steps_pt)
         pts[name] = {"tau": tau, "fps": fps, "speedup_vs_dense": fps / dfps, "ms_per_step": float(np.mean(ms)),
                      **{k: c[k] for k in ("u_in", "u_conv", "mac_frac", "tiles_processed_frac",
                                           "deviation_vs_dense")}}

@@ -99,9 +99,13 @@ enum {
   DCNN_FLAG_NO_TENSOR_CORES = 1,  /* route every conv through the CUDA-core kernel      */
   DCNN_FLAG_FP32_CACHES = 2,      /* dtype F16: keep x^A, x^T and pool accumulators in
                                      fp32 (deltas stay fp16)                             */
-  DCNN_FLAG_HYBRID_DISPATCH = 4   /* with tensor cores, route tiles with <= 4 active input
-                                     pixels to the CUDA-core kernel;
-                                     default: every non-empty tile on tcgen05             */
+  DCNN_FLAG_HYBRID_DISPATCH = 4,  /* route tiles with 1..4 active input pixels to the
+                                     list-driven very-sparse CUDA-core kernel (PAPER.md:
+                                     283-288); default: every non-empty tile dense (tcgen05
+                                     for fp16, the dense CUDA-core kernel for fp32)        */
+  DCNN_FLAG_PER_PIXEL = 8         /* every non-empty tile list-driven (the paper's "per-pixel
+                                     sparse" mode of Table S1); for
+                                     ablations / the micro-benchmark                      */
 };
 
 typedef struct {

@@ -8,4 +8,4 @@ missing (build it with ``python -m paper_2203_03996_b200.build``).
 from ._lib import (DeltaNet, DcnnError, load_library, OP_CODES, ACT_CODES,  # noqa: F401
                    BUF_DELTA, BUF_MASK, BUF_XA, BUF_XT, BUF_OUT, BUF_POOLA, LIB_PATH,
                    KCLASS_CONV, KCLASS_TILES, KCLASS_POINTWISE, KCLASS_INPUT,
-                   FLAG_NO_TENSOR_CORES, FLAG_FP32_CACHES)
+                   FLAG_NO_TENSOR_CORES, FLAG_FP32_CACHES, FLAG_HYBRID_DISPATCH, FLAG_PER_PIXEL)

@@ -19,6 +19,7 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_UNSUPPORTED", 4: "ERR_N
 FLAG_NO_TENSOR_CORES = 1
 FLAG_FP32_CACHES = 2
 FLAG_HYBRID_DISPATCH = 4
+FLAG_PER_PIXEL = 8
 KCLASS_CONV, KCLASS_TILES, KCLASS_POINTWISE, KCLASS_INPUT = 1, 2, 4, 8
 
 

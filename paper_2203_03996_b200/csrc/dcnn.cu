@@ -70,6 +70,10 @@ struct Op {
   int* list_cc = nullptr;
   int* list_tc = nullptr;
   int cnt_idx = -1;                 // index into counts[] (2 ints per conv)
+  int smax = 0;                     // tiles with 1..smax active inputs run list-driven (a4)
+  int grid_vs = 0;
+  int scan = 0;                     // 1: tiles compacted by k_tile_scan before the conv kernel
+  int scan_off = 0;                 // offset (u64) of its look-back status words
   int grid_cc = 0;
   // tensor-core path (a3)
   bool tc = false;
@@ -103,8 +107,9 @@ struct dcnn_net {
   float* eps = nullptr;             // [n_ops + 1], slot 0 = input
   unsigned long long* stats = nullptr;  // [(n_ops + 1) * 8]; slot 0's active count lives in cta_active
   unsigned long long* cta_active = nullptr;  // [INPUT_MAX_GRID] active input pixels per input-kernel CTA
-  int* counts = nullptr;            // [2 * n_convs]
-  int n_counts = 0;
+  int* counts = nullptr;            // [2 * n_convs] list counts, then the k_tile_scan status words
+  int n_counts = 0;                 // ints zeroed by the input kernel every frame
+  unsigned long long* scan_status = nullptr;
   std::vector<float> eps_host;
   std::vector<void*> allocs;
   // graph; the input-kernel and output-copy nodes get per-call parameters (caller's frame and
@@ -135,6 +140,7 @@ template <typename T>
 static dcnn_status dalloc(dcnn_net* n, T** p, size_t bytes) {
   void* q = nullptr;
   if (bytes == 0) bytes = 16;
+  bytes += 64;                      // tail padding: word-granular mask reads (k_tile_scan) stay in bounds
   CUDA_TRY(cudaMalloc(&q, bytes));
   n->allocs.push_back(q);
   *p = reinterpret_cast<T*>(q);
@@ -200,7 +206,9 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
   Cand best = {1e30, 0, 0, 0, 0, 0, 0};
   for (int ns = 1; ns <= max_split; ns *= 2) {
     if (p.Np % (16 * ns) || p.Np / ns < 16 || p.Np / ns > 256) continue;
-    if (ns > 1 && ntiles * ns > 148) continue;         // all split CTAs in one wave
+    // all split CTAs in one wave (measured: a split that makes clusters walk several tiles
+    // loses to the wider single-wave split -- YOLOv5s S = 8 op 34 143 -> 239 us)
+    if (ns > 1 && ntiles * ns > 148 && !(getenv("DCNN_TC_SPLIT_WAVES"))) continue;
     const int Ns = p.Np / ns;
     const double t_mma = Ns <= 128 ? 0.05 : 0.075;
     const int waves = (ntiles * ns + 147) / 148;
@@ -391,16 +399,25 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       tp.kh = o.kh; tp.kw = o.kw; tp.stride = o.stride; tp.pad = o.pad; tp.dil = o.dil;
       tp.TH = o.TH; tp.TW = o.TW; tp.nty = o.nty; tp.ntx = o.ntx;
       tp.mask_in = src_mask(o.in[0]); tp.mconv = o.mask; tp.first = n->first;
-      // hybrid dispatch: with tensor cores every non-empty tile runs on
-      // tcgen05 unless DCNN_FLAG_HYBRID_DISPATCH routes <= 4-active-input tiles to CUDA cores
-      tp.sparse_max = (n->flags & DCNN_FLAG_HYBRID_DISPATCH) ? 4 : 0; tp.use_tc = o.tc ? 1 : 0;
+      // dispatch: tiles with 1..smax active inputs -> the list-driven
+      // very-sparse kernel (hybrid: smax = 4; per-pixel mode: every non-empty tile), the rest
+      // dense (tcgen05 for fp16, the dense CUDA-core kernel otherwise)
+      tp.sparse_max = o.smax; tp.use_tc = o.tc ? 1 : 0; tp.count_dense = o.tc ? 0 : 1;
       tp.list_cc = o.list_cc; tp.count_cc = n->counts + o.cnt_idx;
       tp.list_tc = o.list_tc; tp.count_tc = n->counts + o.cnt_idx + 1;
       tp.stats = n->stats + (size_t)(i + 1) * 8;
-      const bool fused = o.tc && !(n->flags & DCNN_FLAG_HYBRID_DISPATCH);
-      if (!fused) {                    // tensor-core convs decide their tiles in-kernel
+      // a2: the tcgen05 conv decides its tiles in-kernel (fused scout) unless the layer has
+      // many tiles per CTA; then (and on the CUDA-core path) the compaction kernel builds the lists
+      const bool fused = o.tc && !o.scan;
+      if (!fused) {
         TimeScope ts(n, ost, DCNN_KCLASS_TILES, i);
-        launch_tiles(tp, ost);
+        if (o.scan == 1) {
+          tp.mode = (o.tc && o.smax == 0) ? SCAN_SKIPPED_ZERO : SCAN_MCONV_ALL;
+          tp.status = n->scan_status + o.scan_off;
+          launch_tile_scan(tp, ost);
+        } else {
+          launch_tiles(tp, ost);
+        }
         ++k;
       }
       ConvCCParams cp;
@@ -411,11 +428,19 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       cp.WH = o.WH; cp.WW = o.WW; cp.CIC = o.CIC; cp.PPT = o.PPT;
       cp.delta_in = src_delta(o.in[0]); cp.mask_in = src_mask(o.in[0]);
       cp.wt = o.wt; cp.bias = o.bias;
-      cp.list = o.list_cc; cp.count = n->counts + o.cnt_idx;
       cp.vec = (o.C % 8 == 0) ? 1 : 0;
       cp.G = group_lanes(o.C);
       cp.ep = make_epi(n, i);
-      if (!o.tc || (n->flags & DCNN_FLAG_HYBRID_DISPATCH)) {
+      if (o.smax > 0) {                 // very-sparse tiles (the frame bookkeeping rides on the dense kernel)
+        ConvCCParams vp = cp;
+        vp.list = o.list_cc; vp.count = n->counts + o.cnt_idx;
+        vp.ep.pend_clear = nullptr;
+        TimeScope ts(n, ost, DCNN_KCLASS_CONV, i);
+        launch_conv_vs(vp, n->dtype, n->cache32, o.grid_vs, ost);
+        ++k;
+      }
+      if (!o.tc) {
+        cp.list = o.list_tc; cp.count = n->counts + o.cnt_idx + 1;
         TimeScope ts(n, ost, DCNN_KCLASS_CONV, i);
         launch_conv_cc(cp, n->dtype, n->cache32, o.grid_cc, ost);
         ++k;
@@ -702,8 +727,6 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   CUDA_TRY(cudaMemset(n->stats, 0, sizeof(unsigned long long) * 8 * (L + 1)));
   if ((r = dalloc(n, &n->cta_active, sizeof(unsigned long long) * INPUT_MAX_GRID))) return r;
   CUDA_TRY(cudaMemset(n->cta_active, 0, sizeof(unsigned long long) * INPUT_MAX_GRID));
-  n->n_counts = 2 * n_convs;
-  if ((r = dalloc(n, &n->counts, sizeof(int) * std::max(1, n->n_counts)))) return r;
   CUDA_TRY(cudaMemset(n->first, 1, S));
   CUDA_TRY(cudaMemset(n->pend, 1, S));
   // end-of-frame bookkeeping rides on the first op that consumes the network input: its
@@ -723,7 +746,8 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   n->eps_host[0] = d->input_threshold;
   for (int i = 0; i < L; ++i) n->eps_host[i + 1] = d->layers[i].threshold;
   CUDA_TRY(cudaMemcpy(n->eps, n->eps_host.data(), sizeof(float) * (L + 1), cudaMemcpyHostToDevice));
-  int cnt = 0;
+  int cnt = 0, scan_words = 0;
+  static const bool force_fused = getenv("DCNN_TC_FUSED") != nullptr;   // A/B: in-kernel tile scan only
   std::vector<int> n_consumers(L, 0);
   for (int i = 0; i < L; ++i)
     for (int j = 0; j < n->ops[i].n_in; ++j)
@@ -738,7 +762,8 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
     // its coalesced 16-byte path; outputs are compacted when they are copied out
     o.ld = o.C;
     if (o.kind == DCNN_OP_CONV && o.C % 8 && o.out_slot >= 0 && n_consumers[i] == 0 && o.groups == 1 &&
-        n->dtype == DCNN_F16 && !(n->flags & (DCNN_FLAG_NO_TENSOR_CORES | DCNN_FLAG_HYBRID_DISPATCH)) &&
+        n->dtype == DCNN_F16 &&
+        !(n->flags & (DCNN_FLAG_NO_TENSOR_CORES | DCNN_FLAG_HYBRID_DISPATCH | DCNN_FLAG_PER_PIXEL)) &&
         o.Ci % 16 == 0)
       o.ld = (o.C + 7) / 8 * 8;
     if ((r = dalloc(n, &o.delta, px * o.ld * es))) return r;
@@ -818,7 +843,9 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         CUDA_TRY(cudaMemcpy(o.wtc, w.data(), w.size() * 2, cudaMemcpyHostToDevice));
         p.wtc = o.wtc;
         // pending-residual flags (x^T != 0) for truncating layers on the coalesced fp16 path
-        if (o.act != DCNN_ACT_NONE && !n->cache32 && o.C % 8 == 0 && !(n->flags & DCNN_FLAG_HYBRID_DISPATCH)) {
+        // (not with list-driven tiles: the CUDA-core epilogues keep x^T without the flags)
+        if (o.act != DCNN_ACT_NONE && !n->cache32 && o.C % 8 == 0 &&
+            !(n->flags & (DCNN_FLAG_HYBRID_DISPATCH | DCNN_FLAG_PER_PIXEL))) {
           if ((r = dalloc(n, &p.tflag, S * o.H * o.W))) return r;
           CUDA_TRY(cudaMemset(p.tflag, 0, S * o.H * o.W));
           CUDA_TRY(cudaMemset(o.xT, 0, S * o.H * o.W * o.ld * n->cesz));   // flag 0 <=> x^T == 0
@@ -848,6 +875,9 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         }
         const int ncl = std::max(1, std::min(n->S * o.nty * o.ntx, 148 / p.nsplit));
         o.grid_tc = ncl * p.nsplit;
+        // a2 as a separate compaction kernel when the CTAs' scouts would otherwise walk many
+        // (mostly empty) tiles each: more than two tiles per cluster
+        o.scan = !force_fused && n->S * o.nty * o.ntx > 2 * ncl;
         static const bool show_plan = getenv("DCNN_TC_PLAN") != nullptr;
         if (show_plan)
           fprintf(stderr,
@@ -858,6 +888,30 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
                   conv_tc_smem(p), o.grid_tc, p.sw128);
       }
     }
+    if (o.kind == DCNN_OP_CONV) {
+      o.smax = (n->flags & DCNN_FLAG_PER_PIXEL) ? (1 << 30) : (n->flags & DCNN_FLAG_HYBRID_DISPATCH) ? 4 : 0;
+      if (o.smax) {
+        ConvCCParams q;
+        memset(&q, 0, sizeof(q));
+        q.Ci = o.Ci; q.Co = o.C; q.TH = o.TH; q.TW = o.TW; q.kh = o.kh; q.kw = o.kw; q.stride = o.stride;
+        q.dil = o.dil;
+        if (!conv_vs_ok(q)) o.smax = 0;   // e.g. C % 8 != 0: every non-empty tile dense
+      }
+      o.grid_vs = std::max(1, std::min(n->S * o.nty * o.ntx, 148 * 4));
+      if (!o.tc || o.smax) o.scan = 1;
+      if (o.scan) {
+        TileParams tp;
+        memset(&tp, 0, sizeof(tp));
+        tp.S = n->S; tp.nty = o.nty; tp.ntx = o.ntx; tp.TH = o.TH; tp.TW = o.TW;
+        tp.kh = o.kh; tp.kw = o.kw; tp.stride = o.stride; tp.dil = o.dil;
+        if (!tile_scan_ok(tp)) {
+          o.scan = (o.tc && !o.smax) ? 0 : 2;   // 2: the per-tile block kernel (k_tiles), wide windows
+        } else {
+          o.scan_off = scan_words;
+          scan_words += tile_scan_blocks(tp);
+        }
+      }
+    }
     if (o.kind == DCNN_OP_AFFINE) {
       if ((r = dalloc(n, &o.scale, o.C * 4))) return r;
       if ((r = dalloc(n, &o.shift, o.C * 4))) return r;
@@ -865,7 +919,17 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
       CUDA_TRY(cudaMemcpy(o.shift, ld.shift, o.C * 4, cudaMemcpyHostToDevice));
     }
   }
+  {
+    // list counts + k_tile_scan look-back status words (u64, 8-byte aligned), all zeroed by the
+    // input kernel at the start of every frame
+    const int cnt_ints = (2 * n_convs + 1) / 2 * 2;
+    n->n_counts = cnt_ints + 2 * scan_words;
+    if ((r = dalloc(n, &n->counts, sizeof(int) * std::max(1, n->n_counts)))) return r;
+    CUDA_TRY(cudaMemset(n->counts, 0, sizeof(int) * std::max(1, n->n_counts)));
+    n->scan_status = reinterpret_cast<unsigned long long*>(n->counts + cnt_ints);
+  }
   CUDA_TRY(conv_cc_init());
+  CUDA_TRY(conv_vs_init());
   CUDA_TRY(conv_tc_init());
   CUDA_TRY(cudaStreamCreateWithFlags(&n->cap, cudaStreamNonBlocking));
   {

@@ -1,6 +1,7 @@
 // k_conv_cc.cu -- a2 (mask -> active-tile compaction) and a4 (CUDA-core delta conv).
 //
-// a2: PAPER.md:253-254 (§3.2) "before loading any other data, we first check the
+// a2 (fallback for windows wider than k_tile_scan handles; k_scan.cu is the main path):
+// PAPER.md:253-254 (§3.2) "before loading any other data, we first check the
 // update mask of all input pixels and for an entire tile ... decide whether to
 // skip"; "Independent of whether a tile is skipped, we write the update mask for
 // the subsequent layer".  PAPER.md:283-286: skip (0 active inputs) / very sparse
@@ -65,13 +66,16 @@ __global__ void __launch_bounds__(128) k_tiles(TileParams p) {
       if (s_out == 0) {
         atomicAdd(&st[3], 1ull);                               // skip
       } else {
-        atomicAdd(&st[6], (unsigned long long)s_out);          // m_conv pixels (scaled on host)
-        if (!p.use_tc || s_in <= p.sparse_max) {
+        if (s_in <= p.sparse_max) {                            // very sparse: list-driven kernel
           p.list_cc[atomicAdd(p.count_cc, 1)] = tile;
           atomicAdd(&st[4], 1ull);
+          atomicAdd(&st[6], (unsigned long long)s_out);        // m_conv pixels (scaled on host)
         } else {
           p.list_tc[atomicAdd(p.count_tc, 1)] = tile;
-          atomicAdd(&st[5], 1ull);
+          if (p.count_dense) {                                 // else counted by the tcgen05 conv
+            atomicAdd(&st[5], 1ull);
+            atomicAdd(&st[6], (unsigned long long)s_out);
+          }
         }
       }
     }

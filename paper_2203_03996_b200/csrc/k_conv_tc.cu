@@ -341,11 +341,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     if (lane == 0) {
       info[slot].tile = -1;
       tc::mbar_arrive(&info_full[slot]);
-      if (p.fused && rank == 0 && p.tstats) {
-        atomicAdd(&p.tstats[2], n_tot);
-        atomicAdd(&p.tstats[3], n_skip);
-        atomicAdd(&p.tstats[5], n_dense);
-        atomicAdd(&p.tstats[6], n_mc);
+      if (rank == 0 && p.tstats) {             // list mode: tiles / skips counted by the scan
+        if (p.fused) atomicAdd(&p.tstats[2], n_tot);
+        if (n_skip) atomicAdd(&p.tstats[3], n_skip);
+        if (n_dense) atomicAdd(&p.tstats[5], n_dense);
+        if (n_mc) atomicAdd(&p.tstats[6], n_mc);
       }
     }
   } else if (warp == 8) {
@@ -657,6 +657,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       if (need_cache && coal && actm && C > 0) stage_fill2(gA, gT, n16_of(0), actm, tm);
       if (act && O && !first)
         for (int c = 0; c < C; c += 32) prefetch_l2(O + c);
+      // the later 32-channel slices of the cache rows: into L2 while the MMAs run, so the
+      // epilogue's per-slice round trips (two passes for > 32 channels per thread) hit L2
+      if (need_cache && act && C > 32)
+        for (int c = 32; c < C; c += 32) {
+          prefetch_l2(A + c);
+          if (tpend) prefetch_l2(Tt + c);
+        }
       const int acc = u & 1;
       TCTR(tid == 0 && u == 0, 10);
       tc::mbar_wait(&acc_full[acc], (u >> 1) & 1);

@@ -47,13 +47,24 @@ struct TileParams {
   const uint8_t* mask_in;
   uint8_t* mconv;               // [S,Ho,Wo] receptive-field OR of mask_in (Z7)
   const uint8_t* first;
-  int sparse_max;               // tiles with <= sparse_max active inputs -> CUDA-core list
-  int use_tc;                   // 0: every non-empty tile goes to the CUDA-core list
-  int* list_cc; int* count_cc;  // CUDA-core tiles
-  int* list_tc; int* count_tc;  // tensor-core tiles
+  int sparse_max;               // tiles with 1..sparse_max active inputs -> very-sparse list
+  int use_tc;                   // (k_tiles) dense list consumed by the tcgen05 conv
+  int* list_cc; int* count_cc;  // very-sparse tiles (list-driven CUDA-core kernel)
+  int* list_tc; int* count_tc;  // dense tiles (tcgen05 conv, or the dense CUDA-core conv)
   unsigned long long* stats;    // [active_in, active_out(m_conv), tiles_total, skip, sparse, dense]
+  // k_tile_scan (ballot + prefix scan + decoupled look-back, deterministic list order)
+  int mode;                     // SCAN_MCONV_ALL: write m_conv of every pixel; SCAN_SKIPPED_ZERO:
+                                // write the zero mask of skipped tiles only (tcgen05 epilogue
+                                // writes the active tiles' masks)
+  int WWc;                      // window columns (set by the launcher)
+  unsigned long long* status;   // [blocks] look-back status words, zeroed every frame
+  int count_dense;              // 1: the dense list runs on CUDA cores (the scan counts its tiles)
 };
+enum { SCAN_MCONV_ALL = 0, SCAN_SKIPPED_ZERO = 1 };
 void launch_tiles(const TileParams& p, cudaStream_t st);
+bool tile_scan_ok(const TileParams& p);
+int tile_scan_blocks(const TileParams& p);
+void launch_tile_scan(const TileParams& p, cudaStream_t st);
 
 // ---------------------------------------------------------------- a4: CUDA-core conv
 struct ConvCCParams {
@@ -72,6 +83,10 @@ struct ConvCCParams {
   Epi ep;                       // ep.mask holds m_conv on entry for the tile's pixels
 };
 void launch_conv_cc(const ConvCCParams& p, int dtype, int cache32, int grid, cudaStream_t st);
+// a4 very-sparse mode (k_vsparse.cu): list-driven over the gathered updated inputs of a tile
+void launch_conv_vs(const ConvCCParams& p, int dtype, int cache32, int grid, cudaStream_t st);
+bool conv_vs_ok(const ConvCCParams& p);
+cudaError_t conv_vs_init();
 size_t conv_cc_smem(const ConvCCParams& p);
 cudaError_t conv_cc_init();     // once per process/device: raise the dynamic smem limit
 

@@ -222,3 +222,63 @@ def test_tc_padded_head_rows(co):
         np.testing.assert_array_equal(eng.debug_read(i, BUF_OUT).reshape(out[0].shape), out[0].cpu().numpy())
         assert eng.debug_read(i, BUF_DELTA).size == 24 * 20 * co
     eng.close()
+
+
+@pytest.mark.parametrize("H,W,ci,co,k,s,S", [(20, 20, 256, 512, 3, 1, 4), (20, 20, 128, 256, 1, 1, 6),
+                                           (40, 40, 64, 256, 3, 2, 3)])
+def test_tc_channel_split_multi_tile(H, W, ci, co, k, s, S):
+    """Channel split over a thread-block cluster (DSMEM max-norm exchange) with several tiles
+    per cluster: wide layers of YOLOv5s at S > 1 (both DSMEM exchange slots, TMEM buffer 1)."""
+    net = _single_conv(H, W, ci, co, k, s, 1, "silu", seed=co + k + S)
+    net.layers[0].eps = 0.02
+    rng = np.random.default_rng(S)
+    x = rng.standard_normal((S, H, W, ci)).astype(np.float16)
+    frames = [x]
+    for _ in range(3):
+        ch = rng.random((S, H, W)) < 0.3
+        x = np.where(ch[..., None], rng.standard_normal(x.shape), x).astype(np.float16)
+        frames.append(x)
+    worst = _run(net, np.stack(frames), tol=2e-2, name=f"split_multi_tile_{ci}x{co}_k{k}s{s}_S{S}")
+    print("worst", worst)
+
+
+@pytest.mark.parametrize("hybrid", [False, True])
+@pytest.mark.parametrize("S", [1, 6])
+def test_tile_counters_recount(hybrid, S):
+    """the device tile counters (a2 compaction: ballot + prefix scan, or the fused
+    scout) equal an independent recount from the oracle's masks -- skipped = windows without
+    an active input, hybrid: very sparse = 1..4 active inputs, and the
+    algorithmic MACs = m_conv pixels x K x C_out."""
+    from oracle import DeltaOracle, tile_window_counts
+    from paper_2203_03996_b200 import DeltaNet, FLAG_HYBRID_DISPATCH
+    net = nets.toy_net(96, 80, 32, eps=0.02, dtype="f16")
+    specs = [VideoSpec(96, 80, n_blobs=2, blob_h=9, blob_w=7, speed=3, noise_p=0.002, seed=40 + k) for k in range(S)]
+    fr = clip(specs, 5, np.float16)
+    eng = DeltaNet(net, S, flags=FLAG_HYBRID_DISPATCH if hybrid else 0)
+    orc = DeltaOracle(net, S)
+    outs = [torch.empty((S,) + sh, device="cuda") for sh in eng.out_shapes]
+    convs = [i for i, L in enumerate(net.layers) if L.op == "conv"]
+    for t in range(fr.shape[0]):
+        eng.process_frame(torch.from_numpy(fr[t]).cuda(), outs)
+        torch.cuda.synchronize()
+        from paper_2203_03996_b200 import BUF_MASK
+        force = {i: eng.debug_read(i, BUF_MASK).astype(bool) for i, L in enumerate(net.layers) if L.truncates}
+        orc.step(fr[t], force=force)
+        st = eng.stats()["ops"]
+        for i in convs:
+            L = net.layers[i]
+            src = L.inputs[0]
+            m_in = orc.masks[src]
+            Ho, Wo, _ = eng.op_shape(i)
+            cnt = tile_window_counts(m_in, L.kh, L.kw, L.stride, L.pad, L.dil, Ho, Wo, 16, 8)
+            r = st[i + 1]
+            assert r["tiles_total"] == cnt.size, (t, i)
+            assert r["tiles_skip"] == int((cnt == 0).sum()), (t, i, r, int((cnt == 0).sum()))
+            if hybrid:
+                assert r["tiles_sparse"] == int(((cnt >= 1) & (cnt <= 4)).sum()), (t, i)
+                assert r["tiles_dense"] == int((cnt >= 5).sum()), (t, i)
+            else:
+                assert r["tiles_sparse"] == 0 and r["tiles_dense"] == int((cnt > 0).sum()), (t, i)
+            Ci = eng.op_shape(src)[2]
+            assert r["mac_alg"] == int(orc.conv_masks[i].sum()) * L.kh * L.kw * Ci * L.c_out, (t, i)
+    eng.close()
