@@ -50,6 +50,12 @@ WORKLOADS = {
     "toy": dict(cfg="configs[1]", build=lambda dt: nets.toy_net(128, 128, 64, eps=0.05, dtype=dt),
                 video=dict(H=128, W=128, n_blobs=3, blob_h=22, blob_w=22, speed=3, noise_p=0.01),
                 seed=2, S=1, model="toy5 (conv3x3 3-64+ReLU, maxpool2, conv3x3+ReLU, up2, conv3x3)"),
+    # SURVEY §8(f) NEXT-1 (beside the BASELINE configs): EfficientDet-Lite0 384x384 fp16, the
+    # detection setting of configs[3] (eps_in 0.5 + 7 px dilation, pedestrians)
+    "effdet": dict(cfg="NEXT-1 (EfficientDet-Lite0, SURVEY §8(f); not a BASELINE config)",
+                   build=lambda dt: nets.efficientdet_lite0(dtype=dt),
+                   video=dict(H=384, W=384, n_blobs=8, blob_h=24, blob_w=10, speed=2, noise_p=0.05),
+                   seed=11, S=8, model="EfficientDet-Lite0 384x384 (20 classes)"),
 }
 
 # configs[4] update-rate sweep: pedestrians per frame for u_in ~ 1/2/5/10/20/50 % (SURVEY d2
@@ -58,7 +64,7 @@ SWEEP = [("u~1%", 2, False), ("u~2%", 5, False), ("u~5%", 12, False), ("u~10%", 
          ("u~20%", 55, False), ("u~50%", 170, False), ("u=100% (flicker)", 20, True)]
 
 # beside the headline (N = 1): the other BASELINE workloads and stream counts
-EXTRA = [("hrnet", 1), ("hrnet", 8), ("yolo", 1), ("toy", 1), ("toy", 32)]
+EXTRA = [("hrnet", 1), ("hrnet", 8), ("yolo", 1), ("toy", 1), ("toy", 32), ("effdet", 1), ("effdet", 8)]
 
 
 def peaks():
@@ -131,11 +137,16 @@ def dense_module(net, torch):
             self.b = torch.nn.ParameterList()
             self.idx = {}
             for i, L in enumerate(net.layers):
-                if L.op == "conv":
+                if L.op in ("conv", "convtranspose"):
                     self.idx[i] = len(self.w)
-                    self.w.append(torch.nn.Parameter(torch.from_numpy(L.weight).permute(0, 3, 1, 2).contiguous(),
+                    perm = (0, 3, 1, 2) if L.op == "conv" else (3, 0, 1, 2)
+                    self.w.append(torch.nn.Parameter(torch.from_numpy(L.weight).permute(*perm).contiguous(),
                                                      requires_grad=False))
                     self.b.append(torch.nn.Parameter(torch.from_numpy(L.bias), requires_grad=False))
+                elif L.op == "affine":
+                    self.idx[i] = len(self.w)
+                    self.w.append(torch.nn.Parameter(torch.from_numpy(L.scale).view(1, -1, 1, 1), requires_grad=False))
+                    self.b.append(torch.nn.Parameter(torch.from_numpy(L.shift).view(1, -1, 1, 1), requires_grad=False))
 
         def forward(self, x):
             vals = {}
@@ -150,8 +161,16 @@ def dense_module(net, torch):
                     y = F.max_pool2d(xs[0], L.kh, L.stride, L.pad)
                 elif L.op == "avgpool":
                     y = F.avg_pool2d(xs[0], L.kh, L.stride, L.pad)
+                elif L.op == "convtranspose":
+                    k = self.idx[i]
+                    y = acts[L.act](F.conv_transpose2d(xs[0], self.w[k], self.b[k], L.stride, L.pad))
+                elif L.op == "affine":
+                    k = self.idx[i]
+                    y = xs[0] * self.w[k] + self.b[k]
                 elif L.op == "up":
                     y = F.interpolate(xs[0], scale_factor=L.up, mode="nearest")
+                elif L.op == "upbilinear":
+                    y = F.interpolate(xs[0], scale_factor=L.up, mode="bilinear", align_corners=False)
                 elif L.op == "add":
                     y = acts[L.act](sum(xs))
                 elif L.op == "concat":
@@ -204,7 +223,11 @@ def dense_macs(net):
             shape[i] = (Ho, Wo, L.c_out)
         elif L.op in ("maxpool", "avgpool"):
             shape[i] = ((H + 2 * L.pad - L.kh) // L.stride + 1, (W + 2 * L.pad - L.kh) // L.stride + 1, C)
-        elif L.op == "up":
+        elif L.op == "convtranspose":
+            Ho, Wo = (H - 1) * L.stride - 2 * L.pad + L.kh, (W - 1) * L.stride - 2 * L.pad + L.kw
+            total += H * W * L.c_out * L.kh * L.kw * C          # every input pixel scatters k x k
+            shape[i] = (Ho, Wo, L.c_out)
+        elif L.op in ("up", "upbilinear"):
             shape[i] = (H * L.up, W * L.up, C)
         elif L.op == "concat":
             shape[i] = (H, W, sum(shape[j][2] for j in L.inputs))

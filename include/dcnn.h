@@ -67,7 +67,18 @@ typedef enum {
   DCNN_OP_UPSAMPLE_NEAREST = 4,  /* replicate delta and mask                                    */
   DCNN_OP_ADD = 5,               /* mask union, absent operand = 0; optional fused act+trunc    */
   DCNN_OP_CONCAT = 6,            /* channel concat, mask union, zero-filled inactive operands   */
-  DCNN_OP_AFFINE = 7             /* unfolded BN: dy = scale*dx (+shift on the first frame)      */
+  DCNN_OP_AFFINE = 7,            /* unfolded BN: dy = scale*dx (+shift on the first frame)      */
+  DCNN_OP_UPSAMPLE_BILINEAR = 8, /* x up_factor, align_corners = false; linear: dy = interp of the
+                                    masked source deltas; out mask = any source with weight > 0
+                                    active (inactive sources contribute 0, so no mask pre-dilation
+                                    is needed); NEXT-4                             */
+  DCNN_OP_CONV_TRANSPOSE = 9     /* transposed conv (Pose-ResNet head), groups 1,
+                                    kh == kw, 0 <= pad <= kh-1, no output padding: output
+                                    (H-1)*stride - 2*pad + kh.  weight [c_out][kh][kw][C_in] with
+                                    w[o,ky,kx,i] = torch ConvTranspose2d.weight[i,o,ky,kx].  Linear
+                                    (Eq. 1): run as a zero-insertion of the input delta and mask
+                                    (an internal op) followed by a stride-1 delta conv with the
+                                    flipped kernel; act / threshold / bias as for CONV          */
 } dcnn_op;
 
 /* Activation f of Eq. 5.  act != NONE makes the op a truncation point
@@ -84,7 +95,7 @@ typedef struct {
   int32_t c_out;           /* CONV: output channels                                      */
   int32_t kh, kw;          /* CONV / pools: window                                       */
   int32_t stride, pad, dilation, groups;
-  int32_t up_factor;       /* UPSAMPLE_NEAREST                                           */
+  int32_t up_factor;       /* UPSAMPLE_NEAREST / UPSAMPLE_BILINEAR (integer >= 1)        */
   int32_t act;             /* dcnn_act (CONV, ACT, ADD)                                  */
   float act_param;         /* LEAKY slope (0 -> 0.1)                                      */
   float threshold;         /* eps of Eqs. 4-6: updated iff max_c|dy_c| > eps (strict);

@@ -96,6 +96,36 @@ def conv2d(x, w, b, stride=1, pad=0, dil=1, groups=1):
     return y
 
 
+def conv_transpose2d(x, w, b, stride=1, pad=0):
+    """Transposed convolution by its definition (NEXT-4, the Pose-ResNet head):
+    every input pixel q scatters x[q] * w[:, ky, kx, :] to output p = q * stride - pad + (ky, kx).
+    w [C_out, kh, kw, C_in] (w[o, ky, kx, i] = torch's ConvTranspose2d weight[i, o, ky, kx])."""
+    S, H, W, C = x.shape
+    Co, kh, kw, _ = w.shape
+    Ho, Wo = (H - 1) * stride - 2 * pad + kh, (W - 1) * stride - 2 * pad + kw
+    yp = np.zeros((S, (H - 1) * stride + kh, (W - 1) * stride + kw, Co))   # before cropping the pad
+    for ky in range(kh):
+        for kx in range(kw):
+            yp[:, ky: ky + stride * (H - 1) + 1: stride, kx: kx + stride * (W - 1) + 1: stride, :] += \
+                np.einsum("shwc,oc->shwo", x, w[:, ky, kx, :])
+    y = yp[:, pad: pad + Ho, pad: pad + Wo, :]
+    if b is not None:
+        y = y + b
+    return y
+
+
+def mask_conv_transpose(m, kh, kw, stride=1, pad=0):
+    """Output pixel active iff an active input pixel scatters to it (the receptive-field OR of
+    the transposed conv, Z7)."""
+    S, H, W = m.shape
+    Ho, Wo = (H - 1) * stride - 2 * pad + kh, (W - 1) * stride - 2 * pad + kw
+    yp = np.zeros((S, (H - 1) * stride + kh, (W - 1) * stride + kw), dtype=bool)
+    for ky in range(kh):
+        for kx in range(kw):
+            yp[:, ky: ky + stride * (H - 1) + 1: stride, kx: kx + stride * (W - 1) + 1: stride] |= m
+    return yp[:, pad: pad + Ho, pad: pad + Wo]
+
+
 def mask_conv(m, kh, kw, stride=1, pad=0, dil=1):
     """Output pixel active iff any input pixel in its receptive field is active (Z7);
     padding positions are inactive."""
@@ -137,6 +167,39 @@ def upsample_nearest(x, f):
     return np.repeat(np.repeat(x, f, axis=1), f, axis=2)
 
 
+def _bilinear_taps(n_in, f):
+    """Source taps of every output coordinate of a x f bilinear upsampling along one axis,
+    align_corners = False (the torch / OpenCV convention): src = max(0, (o + 0.5) / f - 0.5),
+    i0 = floor(src), i1 = min(i0 + 1, n_in - 1), weights (1 - l, l) with l = src - i0."""
+    o = np.arange(n_in * f, dtype=np.float64)
+    src = np.maximum((o + 0.5) / f - 0.5, 0.0)
+    i0 = np.floor(src).astype(np.int64)
+    i1 = np.minimum(i0 + 1, n_in - 1)
+    lam = src - i0
+    return i0, i1, 1.0 - lam, lam
+
+
+def upsample_bilinear(x, f):
+    """x f bilinear upsampling of [S,H,W,C], align_corners = False (NEXT-4; PAPER.md:309 lists
+    upsampling layers among the sparse ops): rows, then columns, in fp64."""
+    S, H, W, C = x.shape
+    y0, y1, wy0, wy1 = _bilinear_taps(H, f)
+    x0, x1, wx0, wx1 = _bilinear_taps(W, f)
+    r = x[:, y0] * wy0[None, :, None, None] + x[:, y1] * wy1[None, :, None, None]
+    return r[:, :, x0] * wx0[None, None, :, None] + r[:, :, x1] * wx1[None, None, :, None]
+
+
+def mask_up_bilinear(m, f):
+    """Output pixel active iff a source pixel with a non-zero weight is active (Z11-b): the
+    delta of an interpolated value is the interpolation of the source deltas (linear), and
+    inactive sources contribute exactly 0."""
+    S, H, W = m.shape
+    y0, y1, _, wy1 = _bilinear_taps(H, f)
+    x0, x1, _, wx1 = _bilinear_taps(W, f)
+    rows = m[:, y0] | (m[:, y1] & (wy1 > 0)[None, :, None])
+    return rows[:, :, x0] | (rows[:, :, x1] & (wx1 > 0)[None, None, :])
+
+
 def dilate_chebyshev(m, r):
     """True iff an active pixel lies within Chebyshev distance <= r (clipped; Z4)."""
     if r <= 0:
@@ -168,6 +231,9 @@ def dense_forward(net, frames, wdtype=None):
         if L.op == "conv":
             w, b = _weights(L, wdtype)
             y = act_fn(L.act, conv2d(xs[0], w, b, L.stride, L.pad, L.dil, L.groups))
+        elif L.op == "convtranspose":
+            w, b = _weights(L, wdtype)
+            y = act_fn(L.act, conv_transpose2d(xs[0], w, b, L.stride, L.pad))
         elif L.op == "act":
             y = act_fn(L.act, xs[0])
         elif L.op == "maxpool":
@@ -176,6 +242,8 @@ def dense_forward(net, frames, wdtype=None):
             y = avgpool2d(xs[0], L.kh, L.stride, L.pad)
         elif L.op == "up":
             y = upsample_nearest(xs[0], L.up)
+        elif L.op == "upbilinear":
+            y = upsample_bilinear(xs[0], L.up)
         elif L.op == "add":
             y = act_fn(L.act, sum(xs))
         elif L.op == "concat":
@@ -340,6 +408,19 @@ class DeltaOracle:
                     d, mo = self._truncate(i, z, mo, L.eps, L.act, first)
                 else:
                     d = self._q(z)
+            elif L.op == "convtranspose":
+                dx, mi = ins[0]
+                w, b = _weights(L, self.dt)
+                z = conv_transpose2d(np.where(mi[..., None], dx, 0.0), w, None, L.stride, L.pad)   # linear
+                z = z + np.where(fb[..., None], b, 0.0)                # bias on frame 0 (Z6)
+                mo = mask_conv_transpose(mi, L.kh, L.kw, L.stride, L.pad) | fb
+                if self.record:
+                    self.conv_masks[i] = mo
+                z = np.where(mo[..., None], z, 0.0)
+                if L.truncates:
+                    d, mo = self._truncate(i, z, mo, L.eps, L.act, first)
+                else:
+                    d = self._q(z)
             elif L.op == "act":
                 dx, mi = ins[0]
                 d, mo = self._truncate(i, np.where(mi[..., None], dx, 0.0), mi | fb, L.eps,
@@ -364,6 +445,11 @@ class DeltaOracle:
                 dx, mi = ins[0]
                 d = upsample_nearest(dx, L.up)
                 mo = upsample_nearest(mi[..., None], L.up)[..., 0]
+            elif L.op == "upbilinear":
+                dx, mi = ins[0]
+                mo = mask_up_bilinear(mi, L.up) | fb
+                d = np.where(mo[..., None],
+                             self._q(upsample_bilinear(np.where(mi[..., None], dx, 0.0), L.up)), 0.0)
             elif L.op == "affine":
                 dx, mi = ins[0]
                 sh = np.where(fb[..., None], L.shift.astype(np.float64), 0.0)

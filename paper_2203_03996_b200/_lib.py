@@ -10,7 +10,7 @@ LIB_PATH = os.environ.get("DCNN_LIB") or os.path.join(os.path.dirname(os.path.ab
                                                        "libdcnn.so")
 
 OP_CODES = {"conv": 0, "act": 1, "maxpool": 2, "avgpool": 3, "up": 4, "add": 5, "concat": 6,
-            "affine": 7}
+            "affine": 7, "upbilinear": 8, "convtranspose": 9}
 ACT_CODES = {"none": 0, "relu": 1, "silu": 2, "relu6": 3, "leaky": 4, "sigmoid": 5}
 DTYPES = {"f32": 0, "f16": 1}
 BUF_DELTA, BUF_MASK, BUF_XA, BUF_XT, BUF_OUT, BUF_POOLA = range(6)

@@ -226,8 +226,10 @@ __device__ __forceinline__ bool warp_finish_pixel(const Epi& e, long long pix, i
 }
 
 // Group of G lanes (power of two, aligned inside the warp) finishes one pixel;
-// each lane owns 8-channel chunks j = gl, gl+G, ... (C % 8 == 0, C <= 512 when
-// truncating, so at most 2 chunks per lane when G = min(32, pow2 <= C/8)).
+// each lane owns 8-channel chunks j = gl, gl+G, ... (C % 8 == 0).  Truncating with
+// C <= 512 (at most 2 chunks per lane when G = min(32, pow2 <= C/8)): one pass with the
+// chunks in registers; wider (depthwise layers of 672 / 1152 channels): two passes, the
+// first for the pixel's max-norm, the second recomputes zf and writes.
 // zf(j, z[8]) produces the pre-activation delta of chunk j.  All lanes of the
 // warp must call this together (shuffle reduction).
 template <typename T, typename TC, int ACT, typename ZF>
@@ -242,6 +244,69 @@ __device__ __forceinline__ bool group_finish_pixel(const Epi& e, long long pix, 
   if constexpr (ACT != ACT_NONE) {
     TC* A = reinterpret_cast<TC*>(e.xA) + pix * C;
     TC* Tt = reinterpret_cast<TC*>(e.xT) + pix * C;
+    if (nch > 2 * G) {
+      float mx = 0.f;
+      for (int j = gl; valid && j < nch; j += G) {        // pass 1: max-norm (Eq. 4)
+        float z[8], a[8], t[8];
+        zf(j, z);
+        if (first) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) a[k] = t[k] = 0.f;
+        } else {
+          ld8(A + 8 * j, a);
+          ld8(Tt + 8 * j, t);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float prev = first ? 0.f : act_n<T, ACT>(a[k], e.act_param);
+          mx = fmaxf(mx, fabsf(act_n<T, ACT>(a[k] + t[k] + z[k], e.act_param) - prev));
+        }
+      }
+      for (int o = G >> 1; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float eps = *e.eps;
+      upd = valid && (first || eps < 0.f || mx > eps);
+      for (int j = gl; valid && j < nch; j += G) {        // pass 2: Eqs. 4-6
+        float z[8], a[8], t[8];
+        zf(j, z);
+        if (first) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) a[k] = t[k] = 0.f;
+        } else {
+          ld8(A + 8 * j, a);
+          ld8(Tt + 8 * j, t);
+        }
+        if (upd) {
+          float sv[8], dv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            sv[k] = a[k] + t[k] + z[k];
+            const float prev = first ? 0.f : act_n<T, ACT>(a[k], e.act_param);
+            dv[k] = rnd<T>(act_n<T, ACT>(sv[k], e.act_param) - prev);
+          }
+          st8(A + 8 * j, sv);
+          st8_zero(Tt + 8 * j);
+          st8(dl + 8 * j, dv);
+          if (O) {
+            float o8[8];
+            if (first) {
+              st8(O + 8 * j, dv);
+            } else {
+              ld8(O + 8 * j, o8);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) o8[k] += dv[k];
+              st8(O + 8 * j, o8);
+            }
+          }
+        } else {
+          float tv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) tv[k] = t[k] + z[k];
+          st8(Tt + 8 * j, tv);
+        }
+      }
+      if (valid && gl == 0) e.mask[pix] = upd ? 1 : 0;
+      return upd;
+    }
     float z[2][8], a[2][8], t[2][8];
     float mx = 0.f;
 #pragma unroll

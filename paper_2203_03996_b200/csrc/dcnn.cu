@@ -67,6 +67,11 @@ struct Op {
   int Cp = 0, K = 0;
   int ld = 0;                       // channel pitch of delta / O / caches rows (>= C; see create)
   int TH = 8, TW = 8, nty = 0, ntx = 0, STH = 8, STW = 8, WH = 0, WW = 0, CIC = 0, PPT = 1;
+  // tiling geometry of a conv: streams, output rows/cols, input rows/cols.  Normally (S, H, W,
+  // Hi, Wi); a "flat" 1x1 stride-1 tensor-core conv views each stream's map as H*W/8 rows x 8
+  // columns, so a 16x8 tile is 128 consecutive pixels of one stream (a 1x1 conv has no
+  // neighbourhood; only the ragged end of each stream's map is wasted)
+  int tS = 0, tH = 0, tW = 0, tHi = 0, tWi = 0, flat = 0;
   int* list_cc = nullptr;
   int* list_tc = nullptr;
   int cnt_idx = -1;                 // index into counts[] (2 ints per conv)
@@ -90,7 +95,9 @@ struct Op {
 struct dcnn_net {
   int device = 0, S = 1, dtype = 0, esz = 4, cache32 = 0, cesz = 4;
   int inH = 0, inW = 0, inC = 0, inCp = 0, radius = 0, flags = 0;
-  std::vector<Op> ops;
+  std::vector<Op> ops;              // internal ops (a CONV_TRANSPOSE layer is two of them)
+  std::vector<int> umap;            // caller's layer index -> internal op index
+  std::vector<int> uinv;            // internal op index -> caller's layer index
   std::vector<int> outputs;
   // device state
   void* frame_in = nullptr;
@@ -182,15 +189,16 @@ static dcnn_status plan_cc(Op& o) {
 //                                  further channel (two passes), + 1.0 for the DSMEM exchange
 // and the cheapest one is taken: tile latency = max(halo pipeline, weight pipeline, MMAs)
 // + epilogue, plus the extra tiles a CTA runs when the tiles exceed one wave.
-static bool plan_tc(Op& o, int dtype, int flags, int S) {
+static bool plan_tc(Op& o, int dtype, int flags) {
   if (dtype != DCNN_F16 || (flags & DCNN_FLAG_NO_TENSOR_CORES)) return false;
-  if (o.Ci % 16 || o.C > 512) return false;
+  if (o.Ci % 16 || o.C > 2048) return false;
   ConvTCParams& p = o.tcp;
   memset(&p, 0, sizeof(p));
   p.Np = (o.C + 15) / 16 * 16;
-  const int ntiles = S * ((o.H + 15) / 16) * ((o.W + 7) / 8);
+  const int ntiles = o.tS * ((o.tH + 15) / 16) * ((o.tW + 7) / 8);
   static const int max_split = getenv("DCNN_TC_MAX_SPLIT") ? atoi(getenv("DCNN_TC_MAX_SPLIT")) : 8;
   static const bool no_resident = getenv("DCNN_TC_NO_RESIDENT") != nullptr;
+  static const int force_nab = getenv("DCNN_TC_NAB") ? atoi(getenv("DCNN_TC_NAB")) : 0;   // A/B: halo buffers
   p.dbg = getenv("DCNN_TC_DBG") ? atoi(getenv("DCNN_TC_DBG")) : 0;
   const int s = o.stride, d = o.dil;
   if (s > 2 || o.kh * o.kw > 64) return false;         // stride phases / tap table
@@ -204,7 +212,10 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
   const int plane = (p.HH * p.WQ * 16 + 127) / 128 * 128;
   struct Cand { double cost; int ns, BK, tg, stages, nab, resident; };
   Cand best = {1e30, 0, 0, 0, 0, 0, 0};
-  for (int ns = 1; ns <= max_split; ns *= 2) {
+  // power-of-two splits first; 3, 5, 6, 7 only when none fits (e.g. 672 = 3 x 224 channels)
+  for (int pass = 0; pass < 2 && best.ns == 0; ++pass)
+  for (int ns = 1; ns <= max_split; ++ns) {
+    if (((ns & (ns - 1)) == 0) != (pass == 0)) continue;
     if (p.Np % (16 * ns) || p.Np / ns < 16 || p.Np / ns > 256) continue;
     // all split CTAs in one wave (measured: a split that makes clusters walk several tiles
     // loses to the wider single-wave split -- YOLOv5s S = 8 op 34 143 -> 239 us)
@@ -231,6 +242,7 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
           if (resident && nsteps > 16) continue;
           for (int nab = 2; nab <= 4; ++nab) {
             if (nab > 2 && nab > ncb) break;
+            if (force_nab && nab != std::min(force_nab, std::max(2, ncb))) continue;
             double wb;
             int stages;
             if (resident) {
@@ -262,6 +274,7 @@ static bool plan_tc(Op& o, int dtype, int flags, int S) {
   if (best.ns == 0) return false;
   static const bool no_sw = getenv("DCNN_TC_NO_SW128") != nullptr;
   p.sw128 = (!no_sw && o.kh == 1 && o.kw == 1 && s == 1 && best.BK == 64) ? 1 : 0;
+
   p.nsplit = best.ns;
   p.Ns = p.Np / best.ns;
   p.BK = best.BK;
@@ -395,7 +408,7 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
     cudaStream_t ost = stream_of(sidx);
     if (o.kind == DCNN_OP_CONV) {
       TileParams tp;
-      tp.S = n->S; tp.H = o.Hi; tp.W = o.Wi; tp.Ho = o.H; tp.Wo = o.W;
+      tp.S = o.tS; tp.H = o.tHi; tp.W = o.tWi; tp.Ho = o.tH; tp.Wo = o.tW;
       tp.kh = o.kh; tp.kw = o.kw; tp.stride = o.stride; tp.pad = o.pad; tp.dil = o.dil;
       tp.TH = o.TH; tp.TW = o.TW; tp.nty = o.nty; tp.ntx = o.ntx;
       tp.mask_in = src_mask(o.in[0]); tp.mconv = o.mask; tp.first = n->first;
@@ -452,7 +465,7 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
         p.list = o.list_tc;
         p.count = n->counts + o.cnt_idx + 1;
         p.fused = fused ? 1 : 0;
-        p.ntiles = n->S * o.nty * o.ntx;
+        p.ntiles = o.tS * o.nty * o.ntx;
         p.tstats = n->stats + (size_t)(i + 1) * 8;
         p.ep = make_epi(n, i);
         TimeScope ts(n, ost, DCNN_KCLASS_CONV, i);
@@ -471,6 +484,8 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       }
       pp.k = o.kh; pp.stride = o.stride; pp.pad = o.pad; pp.up = o.up;
       pp.scale = o.scale; pp.shift = o.shift; pp.poolA = o.poolA;
+      pp.dil = o.dil; pp.wdw = o.wt; pp.bdw = o.bias;
+      pp.mconv = n->stats + (size_t)(i + 1) * 8 + 6;
       bool vec = o.C % 8 == 0;
       if (o.kind == DCNN_OP_CONCAT)
         for (int j = 0; j < o.n_in; ++j) vec = vec && o.Cin[j] % 8 == 0;
@@ -608,7 +623,8 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
     const dcnn_layer_desc& ld = d->layers[i];
     Op& o = n->ops[i];
     o.kind = ld.op;
-    if (ld.op < DCNN_OP_CONV || ld.op > DCNN_OP_AFFINE) return fail(DCNN_ERR_ARG, "layer " + std::to_string(i) + ": bad op");
+    if ((ld.op < DCNN_OP_CONV || ld.op > DCNN_OP_UPSAMPLE_BILINEAR) && ld.op != OP_ZERO_INSERT)
+      return fail(DCNN_ERR_ARG, "layer " + std::to_string(i) + ": bad op");
     o.n_in = (ld.op == DCNN_OP_ADD || ld.op == DCNN_OP_CONCAT) ? ld.n_in : 1;
     if (o.n_in < 1 || o.n_in > 4) return fail(DCNN_ERR_ARG, "layer " + std::to_string(i) + ": n_in");
     for (int j = 0; j < o.n_in; ++j) {
@@ -632,6 +648,13 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         o.H = conv_out(o.Hi, o.kh, o.stride, o.pad, o.dil);
         o.W = conv_out(o.Wi, o.kw, o.stride, o.pad, o.dil);
         ++n_convs;
+        {
+          // depthwise (groups == C_in == C_out): the per-pixel sparse CUDA-core kernel of
+          // PAPER.md:661-667 instead of dense-expanded groups
+          static const bool no_dw = getenv("DCNN_NO_DEPTHWISE") != nullptr;
+          if (!no_dw && o.groups > 1 && o.groups == o.Ci && o.C == o.Ci && o.kh == o.kw && o.C % 8 == 0)
+            o.kind = KIND_DEPTHWISE;
+        }
         break;
       }
       case DCNN_OP_ACT:
@@ -647,7 +670,12 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         o.C = o.Ci; o.dil = 1;
         if (o.act) return fail(DCNN_ERR_UNSUPPORTED, "pool with fused act");
         break;
+      case OP_ZERO_INSERT:              // internal (CONV_TRANSPOSE): x[q] -> x'[q * up], zeros between
+        if (o.up < 1) return fail(DCNN_ERR_ARG, "stride");
+        o.H = (o.Hi - 1) * o.up + 1; o.W = (o.Wi - 1) * o.up + 1; o.C = o.Ci;
+        break;
       case DCNN_OP_UPSAMPLE_NEAREST:
+      case DCNN_OP_UPSAMPLE_BILINEAR:
         if (o.up < 1) return fail(DCNN_ERR_ARG, "up_factor");
         o.H = o.Hi * o.up; o.W = o.Wi * o.up; o.C = o.Ci;
         if (o.act) return fail(DCNN_ERR_UNSUPPORTED, "upsample with fused act");
@@ -679,7 +707,12 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         break;
     }
     if (o.H <= 0 || o.W <= 0 || o.C <= 0) return fail(DCNN_ERR_SHAPE, "layer " + std::to_string(i) + ": empty output");
-    if (o.act != DCNN_ACT_NONE && o.C > 32 * MAXK) return fail(DCNN_ERR_UNSUPPORTED, "truncating op with more than 512 channels");
+    // wider truncating layers: depthwise (two-pass group epilogue) and fp16 tensor-core convs (channel
+    // split over a cluster; checked again once the conv is planned)
+    const bool wide_ok = o.kind == KIND_DEPTHWISE ||
+                         (o.kind == DCNN_OP_CONV && n->dtype == DCNN_F16 && o.C % 8 == 0 && o.C <= 2048);
+    if (o.act != DCNN_ACT_NONE && o.C > 32 * MAXK && !wide_ok)
+      return fail(DCNN_ERR_UNSUPPORTED, "truncating op with more than 512 channels");
   }
   // pad the input delta's channels to 16 when every consumer of the input is a
   // dense conv that can then run on the tensor cores (zero channels, zero weights)
@@ -778,14 +811,31 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
       CUDA_TRY(cudaMemset(o.O, 0, px * o.ld * sizeof(float)));
     }
     if (o.kind == DCNN_OP_CONV) {
-      if ((r = plan_cc(o))) return r;
-      o.tc = plan_tc(o, n->dtype, n->flags, n->S);
+      if (o.C <= 32 * MAXK && (r = plan_cc(o))) return r;   // (wider: tensor cores only)
+      o.tS = S; o.tH = o.H; o.tW = o.W; o.tHi = o.Hi; o.tWi = o.Wi;
+      {
+        // flat tiling for 1x1 stride-1 convs whose maps leave ragged 16x8 tiles (e.g. YOLOv5s
+        // 20x20: 6 spatial tiles per stream for 3.1 tiles' worth of pixels -> 4); tensor-core only
+        static const bool no_flat = getenv("DCNN_TC_NO_FLAT") != nullptr;
+        const long long hw = (long long)o.H * o.W;
+        const long long spatial = (long long)((o.H + 15) / 16) * ((o.W + 7) / 8), flat = (hw + 127) / 128;
+        if (!no_flat && o.kh == 1 && o.kw == 1 && o.stride == 1 && o.pad == 0 && o.groups == 1 && hw % 8 == 0 &&
+            hw / 8 < (1ll << 30) && 10 * flat < 9 * spatial &&
+            !(n->flags & (DCNN_FLAG_HYBRID_DISPATCH | DCNN_FLAG_PER_PIXEL))) {
+          o.tH = o.tHi = (int)(hw / 8); o.tW = o.tWi = 8;
+          o.flat = 1;
+        }
+      }
+      o.tc = plan_tc(o, n->dtype, n->flags);
+      if (!o.tc && o.flat) { o.tS = S; o.tH = o.H; o.tW = o.W; o.tHi = o.Hi; o.tWi = o.Wi; o.flat = 0; }
+      if (!o.tc && o.act != DCNN_ACT_NONE && o.C > 32 * MAXK)
+        return fail(DCNN_ERR_UNSUPPORTED, "conv " + std::to_string(i) + ": more than 512 channels needs the tensor-core path");
       if (!o.tc && o.ld != o.C) return fail(DCNN_ERR_UNSUPPORTED, "conv " + std::to_string(i) + ": padded head without tensor-core plan");
       if (o.tc) { o.TH = 16; o.TW = 8; }
       o.K = o.kh * o.kw * (o.Ci_real / o.groups);
-      o.nty = (o.H + o.TH - 1) / o.TH;
-      o.ntx = (o.W + o.TW - 1) / o.TW;
-      const int ntiles = n->S * o.nty * o.ntx;
+      o.nty = (o.tH + o.TH - 1) / o.TH;
+      o.ntx = (o.tW + o.TW - 1) / o.TW;
+      const int ntiles = o.tS * o.nty * o.ntx;
       if ((r = dalloc(n, &o.list_cc, sizeof(int) * ntiles))) return r;
       if ((r = dalloc(n, &o.list_tc, sizeof(int) * ntiles))) return r;
       o.cnt_idx = cnt;
@@ -816,7 +866,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
       if (smem > 200 * 1024) return fail(DCNN_ERR_UNSUPPORTED, "conv tile does not fit shared memory");
       if (o.tc) {
         ConvTCParams& p = o.tcp;
-        p.S = n->S; p.H = o.Hi; p.W = o.Wi; p.Ci = o.Ci; p.Ho = o.H; p.Wo = o.W; p.Co = o.C;
+        p.S = o.tS; p.H = o.tHi; p.W = o.tWi; p.Ci = o.Ci; p.Ho = o.tH; p.Wo = o.tW; p.Co = o.C;
         p.kh = o.kh; p.kw = o.kw; p.stride = o.stride; p.pad = o.pad; p.dil = o.dil;
         p.nty = o.nty; p.ntx = o.ntx;
         p.bias = o.bias;
@@ -849,6 +899,15 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
           if ((r = dalloc(n, &p.tflag, S * o.H * o.W))) return r;
           CUDA_TRY(cudaMemset(p.tflag, 0, S * o.H * o.W));
           CUDA_TRY(cudaMemset(o.xT, 0, S * o.H * o.W * o.ld * n->cesz));   // flag 0 <=> x^T == 0
+          // single-pass truncation: x^A double-buffered per pixel (not for output ops, whose
+          // O += delta needs the decision before the delta is final)
+          // (only where an epilogue thread holds > 32 channels, i.e. Ns > 64: with fewer, the
+          // single pass that stages both outcomes in shared memory writes fewer bytes)
+          static const bool no_dbl = getenv("DCNN_TC_NO_DBL") != nullptr;
+          if (!no_dbl && o.out_slot < 0 && p.Ns > 64) {
+            if ((r = dalloc(n, &p.xA2, px * o.ld * n->cesz))) return r;
+            CUDA_TRY(cudaMemset(p.xA2, 0, px * o.ld * n->cesz));
+          }
         }
         // TMA view of the input delta [S][Hi][Wi][Ci] fp16: dims (C, x, y, stream); a box is
         // 8 channels x one stride phase of the halo columns x all halo rows
@@ -862,9 +921,9 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
             encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
           }
           void* src = o.in[0] < 0 ? n->in_delta : n->ops[o.in[0]].delta;
-          const cuuint64_t gdim[4] = {(cuuint64_t)o.Ci, (cuuint64_t)o.Wi, (cuuint64_t)o.Hi, (cuuint64_t)n->S};
-          const cuuint64_t gstr[3] = {(cuuint64_t)o.Ci * 2, (cuuint64_t)o.Wi * o.Ci * 2,
-                                      (cuuint64_t)o.Hi * o.Wi * o.Ci * 2};
+          const cuuint64_t gdim[4] = {(cuuint64_t)o.Ci, (cuuint64_t)o.tWi, (cuuint64_t)o.tHi, (cuuint64_t)o.tS};
+          const cuuint64_t gstr[3] = {(cuuint64_t)o.Ci * 2, (cuuint64_t)o.tWi * o.Ci * 2,
+                                      (cuuint64_t)o.tHi * o.tWi * o.Ci * 2};
           const cuuint32_t box[4] = {p.sw128 ? 64u : 8u, (cuuint32_t)(o.stride * p.WQ), (cuuint32_t)p.HH, 1};
           const cuuint32_t es[4] = {1, (cuuint32_t)o.stride, 1, 1};
           CUresult cr = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, src, gdim, gstr, box, es,
@@ -873,17 +932,17 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
           if (cr != CUDA_SUCCESS) return fail(DCNN_ERR_CUDA, "conv " + std::to_string(i) + ": tensor map encode failed");
         }
-        const int ncl = std::max(1, std::min(n->S * o.nty * o.ntx, 148 / p.nsplit));
+        const int ncl = std::max(1, std::min(o.tS * o.nty * o.ntx, 148 / p.nsplit));
         o.grid_tc = ncl * p.nsplit;
         // a2 as a separate compaction kernel when the CTAs' scouts would otherwise walk many
         // (mostly empty) tiles each: more than two tiles per cluster
-        o.scan = !force_fused && n->S * o.nty * o.ntx > 2 * ncl;
+        o.scan = !force_fused && o.tS * o.nty * o.ntx > 2 * ncl;
         static const bool show_plan = getenv("DCNN_TC_PLAN") != nullptr;
         if (show_plan)
           fprintf(stderr,
                   "[dcnn plan] op %d %dx%dx%d->%dx%dx%d k%d s%d: tiles %d nsplit %d Ns %d BK %d ncb %d tg %d steps %d "
                   "stages %d resident %d halo_bufs %d a_bytes %d b_bytes %d smem %zu grid %d sw128 %d\n",
-                  i, o.Hi, o.Wi, o.Ci, o.H, o.W, o.C, o.kh, o.stride, n->S * o.nty * o.ntx, p.nsplit, p.Ns, p.BK,
+                  i, o.Hi, o.Wi, o.Ci, o.H, o.W, o.C, o.kh, o.stride, o.tS * o.nty * o.ntx, p.nsplit, p.Ns, p.BK,
                   p.ncb, p.tg, p.ncb * (o.kh * o.kw / p.tg), p.stages, p.resident, p.n_abuf, p.a_bytes, p.b_bytes,
                   conv_tc_smem(p), o.grid_tc, p.sw128);
       }
@@ -897,12 +956,12 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         q.dil = o.dil;
         if (!conv_vs_ok(q)) o.smax = 0;   // e.g. C % 8 != 0: every non-empty tile dense
       }
-      o.grid_vs = std::max(1, std::min(n->S * o.nty * o.ntx, 148 * 4));
+      o.grid_vs = std::max(1, std::min(o.tS * o.nty * o.ntx, 148 * 4));
       if (!o.tc || o.smax) o.scan = 1;
       if (o.scan) {
         TileParams tp;
         memset(&tp, 0, sizeof(tp));
-        tp.S = n->S; tp.nty = o.nty; tp.ntx = o.ntx; tp.TH = o.TH; tp.TW = o.TW;
+        tp.S = o.tS; tp.nty = o.nty; tp.ntx = o.ntx; tp.TH = o.TH; tp.TW = o.TW;
         tp.kh = o.kh; tp.kw = o.kw; tp.stride = o.stride; tp.dil = o.dil;
         if (!tile_scan_ok(tp)) {
           o.scan = (o.tc && !o.smax) ? 0 : 2;   // 2: the per-tile block kernel (k_tiles), wide windows
@@ -911,6 +970,22 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
           scan_words += tile_scan_blocks(tp);
         }
       }
+    }
+    if (o.kind == KIND_DEPTHWISE) {
+      // weights OHWI [C][k][k][1] -> [k*k][C] fp32, values rounded to the storage dtype
+      o.K = o.kh * o.kw;
+      std::vector<float> w((size_t)o.kh * o.kw * o.C), b(o.C, 0.f);
+      for (int c = 0; c < o.C; ++c)
+        for (int t = 0; t < o.kh * o.kw; ++t) {
+          float v = ld.weight[(size_t)c * o.kh * o.kw + t];
+          if (n->dtype == DCNN_F16) v = __half2float(__float2half_rn(v));
+          w[(size_t)t * o.C + c] = v;
+        }
+      if (ld.bias) std::copy(ld.bias, ld.bias + o.C, b.begin());
+      if ((r = dalloc(n, &o.wt, w.size() * 4))) return r;
+      CUDA_TRY(cudaMemcpy(o.wt, w.data(), w.size() * 4, cudaMemcpyHostToDevice));
+      if ((r = dalloc(n, &o.bias, o.C * 4))) return r;
+      CUDA_TRY(cudaMemcpy(o.bias, b.data(), o.C * 4, cudaMemcpyHostToDevice));
     }
     if (o.kind == DCNN_OP_AFFINE) {
       if ((r = dalloc(n, &o.scale, o.C * 4))) return r;
@@ -956,8 +1031,94 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
 dcnn_status dcnn_create_net(const dcnn_net_desc* desc, dcnn_net** out) {
   if (!desc || !out) return fail(DCNN_ERR_ARG, "null argument");
   *out = nullptr;
+  if (desc->in_h <= 0 || desc->in_w <= 0 || desc->in_c <= 0 || desc->n_streams <= 0 || desc->n_layers <= 0 ||
+      !desc->layers || desc->n_outputs <= 0 || !desc->output_ops) {
+    dcnn_net tmp;                       // argument / shape errors, reported in create_impl's order
+    return create_impl(desc, &tmp);
+  }
+  // lowering: a transposed conv (stride s, pad p, k x k) = zero-insertion of its input (s - 1
+  // zeros between pixels; inserted pixels inactive) + a stride-1 conv with pad k - 1 - p and the
+  // spatially flipped kernel (the two are equal by Eq. 1's linearity, term by term)
+  const int Lu = desc->n_layers;
+  std::vector<dcnn_layer_desc> ex;
+  std::vector<std::vector<float>> wflip;
+  std::vector<int> umap(Lu), uinv;
+  wflip.reserve(Lu);
+  for (int i = 0; i < Lu; ++i) {
+    dcnn_layer_desc d = desc->layers[i];
+    const int nin = (d.op == DCNN_OP_ADD || d.op == DCNN_OP_CONCAT) ? d.n_in : 1;
+    for (int j = 0; j < nin && j < 4; ++j)
+      if (d.in[j] >= 0 && d.in[j] < i) d.in[j] = umap[d.in[j]];
+      else if (d.in[j] >= i) return fail(DCNN_ERR_SHAPE, "layer " + std::to_string(i) + ": dangling input reference");
+    if (d.op == DCNN_OP_CONV_TRANSPOSE) {
+      if (d.kh <= 0 || d.kh != d.kw || d.stride < 1 || d.pad < 0 || d.pad > d.kh - 1 || d.c_out <= 0)
+        return fail(DCNN_ERR_UNSUPPORTED, "conv_transpose " + std::to_string(i) + ": needs kh == kw, stride >= 1, 0 <= pad <= kh-1");
+      if ((d.groups != 1 && d.groups != 0) || (d.dilation != 1 && d.dilation != 0))
+        return fail(DCNN_ERR_UNSUPPORTED, "conv_transpose " + std::to_string(i) + ": groups / dilation must be 1");
+      if (!d.weight) return fail(DCNN_ERR_ARG, "conv_transpose " + std::to_string(i) + ": no weights");
+      int Ci = 0;                       // input channels: walk the expanded descs
+      {
+        const int src = d.in[0];
+        int c = desc->in_c;
+        std::vector<int> ch(ex.size());
+        for (size_t k = 0; k < ex.size(); ++k) {
+          const dcnn_layer_desc& e = ex[k];
+          int cin0 = e.in[0] < 0 ? desc->in_c : ch[e.in[0]];
+          if (e.op == DCNN_OP_CONV) ch[k] = e.c_out;
+          else if (e.op == DCNN_OP_CONCAT) {
+            int t = 0;
+            for (int j = 0; j < e.n_in; ++j) t += e.in[j] < 0 ? desc->in_c : ch[e.in[j]];
+            ch[k] = t;
+          } else ch[k] = cin0;
+        }
+        Ci = src < 0 ? c : ch[src];
+      }
+      dcnn_layer_desc z;
+      memset(&z, 0, sizeof(z));
+      z.op = OP_ZERO_INSERT;
+      z.n_in = 1;
+      z.in[0] = d.in[0];
+      z.up_factor = d.stride;
+      z.threshold = 0.f;
+      ex.push_back(z);
+      uinv.push_back(i);
+      const int k = d.kh;
+      wflip.emplace_back((size_t)d.c_out * k * k * Ci);
+      std::vector<float>& w = wflip.back();
+      for (int o = 0; o < d.c_out; ++o)
+        for (int ky = 0; ky < k; ++ky)
+          for (int kx = 0; kx < k; ++kx)
+            for (int c = 0; c < Ci; ++c)
+              w[(((size_t)o * k + ky) * k + kx) * Ci + c] = d.weight[(((size_t)o * k + (k - 1 - ky)) * k + (k - 1 - kx)) * Ci + c];
+      dcnn_layer_desc c = d;
+      c.op = DCNN_OP_CONV;
+      c.in[0] = (int)ex.size() - 1;
+      c.stride = 1;
+      c.pad = k - 1 - d.pad;
+      c.dilation = 1;
+      c.groups = 1;
+      c.weight = w.data();
+      ex.push_back(c);
+    } else {
+      ex.push_back(d);
+    }
+    umap[i] = (int)ex.size() - 1;
+    uinv.push_back(i);
+  }
+  std::vector<int32_t> outs(desc->n_outputs);
+  for (int q = 0; q < desc->n_outputs; ++q) {
+    const int o = desc->output_ops[q];
+    if (o < 0 || o >= Lu) return fail(DCNN_ERR_ARG, "output op index");
+    outs[q] = umap[o];
+  }
+  dcnn_net_desc d2 = *desc;
+  d2.n_layers = (int32_t)ex.size();
+  d2.layers = ex.data();
+  d2.output_ops = outs.data();
   dcnn_net* n = new dcnn_net();
-  dcnn_status s = create_impl(desc, n);
+  n->umap = umap;
+  n->uinv = uinv;
+  dcnn_status s = create_impl(&d2, n);
   if (s != DCNN_OK) {
     std::string keep = g_err;
     dcnn_destroy_net(n);
@@ -970,7 +1131,8 @@ dcnn_status dcnn_create_net(const dcnn_net_desc* desc, dcnn_net** out) {
 
 dcnn_status dcnn_set_threshold(dcnn_net* n, int32_t op, float eps) {
   if (!n) return fail(DCNN_ERR_ARG, "null net");
-  if (op < -1 || op >= (int)n->ops.size()) return fail(DCNN_ERR_ARG, "op index");
+  if (op < -1 || op >= (int)n->umap.size()) return fail(DCNN_ERR_ARG, "op index");
+  if (op >= 0) op = n->umap[op];
   if (op >= 0 && n->ops[op].act == DCNN_ACT_NONE) return fail(DCNN_ERR_ARG, "op has no truncation");
   if (std::isnan(eps)) return fail(DCNN_ERR_ARG, "eps is NaN");
   CUDA_TRY(cudaSetDevice(n->device));
@@ -1069,7 +1231,8 @@ dcnn_status dcnn_process_frame_host(dcnn_net* n, const void* host_frames, void* 
 
 dcnn_status dcnn_op_shape(dcnn_net* n, int32_t op, int32_t* H, int32_t* W, int32_t* C) {
   if (!n || !H || !W || !C) return fail(DCNN_ERR_ARG, "null argument");
-  if (op < -1 || op >= (int)n->ops.size()) return fail(DCNN_ERR_ARG, "op index");
+  if (op < -1 || op >= (int)n->umap.size()) return fail(DCNN_ERR_ARG, "op index");
+  if (op >= 0) op = n->umap[op];
   if (op < 0) { *H = n->inH; *W = n->inW; *C = n->inC; }
   else { *H = n->ops[op].H; *W = n->ops[op].W; *C = n->ops[op].C; }
   return DCNN_OK;
@@ -1095,9 +1258,11 @@ dcnn_status dcnn_get_stats(dcnn_net* n, dcnn_op_stats* per_op, int64_t* frame_in
   if (frame_index) *frame_index = fi;
   if (device_error) *device_error = err ? DCNN_ERR_NONFINITE : DCNN_OK;
   if (per_op) {
-    for (int i = 0; i <= L; ++i) {
+    const int Lu = (int)n->umap.size();
+    for (int u = 0; u <= Lu; ++u) {
+      const int i = u == 0 ? 0 : n->umap[u - 1] + 1;   // internal slot (0 = the input layer)
       const unsigned long long* r = &raw[(size_t)8 * i];
-      dcnn_op_stats& o = per_op[i];
+      dcnn_op_stats& o = per_op[u];
       memset(&o, 0, sizeof(o));
       o.active_out = (int64_t)r[1];
       if (i == 0) {
@@ -1106,6 +1271,9 @@ dcnn_status dcnn_get_stats(dcnn_net* n, dcnn_op_stats* per_op, int64_t* frame_in
       }
       const Op& op = n->ops[i - 1];
       o.active_in = (int64_t)raw[(size_t)8 * (op.in[0] + 1) + 1];
+      if (op.kind == KIND_DEPTHWISE) {             // per-pixel sparse: executed = algorithmic
+        o.mac_alg = o.mac_exec = (int64_t)r[6] * op.K * op.C;
+      }
       if (op.kind == DCNN_OP_CONV) {
         o.tiles_total = (int64_t)r[2];
         o.tiles_skip = (int64_t)r[3];
@@ -1122,7 +1290,8 @@ dcnn_status dcnn_get_stats(dcnn_net* n, dcnn_op_stats* per_op, int64_t* frame_in
 
 dcnn_status dcnn_debug_read(dcnn_net* n, int32_t op, int32_t which, void* host, int64_t* bytes) {
   if (!n) return fail(DCNN_ERR_ARG, "null net");
-  if (op < -1 || op >= (int)n->ops.size()) return fail(DCNN_ERR_ARG, "op index");
+  if (op < -1 || op >= (int)n->umap.size()) return fail(DCNN_ERR_ARG, "op index");
+  if (op >= 0) op = n->umap[op];
   CUDA_TRY(cudaSetDevice(n->device));
   const void* src = nullptr;
   size_t nb = 0;
@@ -1173,6 +1342,28 @@ dcnn_status dcnn_debug_read(dcnn_net* n, int32_t op, int32_t which, void* host, 
       default: return fail(DCNN_ERR_ARG, "which");
     }
     if (!src) return fail(DCNN_ERR_ARG, "buffer not present for this op");
+    if (esz && o.tc && o.tcp.tflag && (which == DCNN_BUF_XA || which == DCNN_BUF_XT)) {
+      // per-pixel state bits (k_conv_tc.cu): bit 1 -> x^A lives in xA2; bit 0 clear -> x^T = 0
+      nb = px * o.C * esz;
+      if (bytes) *bytes = (int64_t)nb;
+      if (!host) return DCNN_OK;
+      CUDA_TRY(cudaDeviceSynchronize());
+      std::vector<uint8_t> fl(px);
+      CUDA_TRY(cudaMemcpy(fl.data(), o.tcp.tflag, px, cudaMemcpyDeviceToHost));
+      std::vector<char> b0(px * o.ld * esz), b1;
+      CUDA_TRY(cudaMemcpy(b0.data(), src, b0.size(), cudaMemcpyDeviceToHost));
+      if (which == DCNN_BUF_XA && o.tcp.xA2) {
+        b1.resize(b0.size());
+        CUDA_TRY(cudaMemcpy(b1.data(), o.tcp.xA2, b1.size(), cudaMemcpyDeviceToHost));
+      }
+      char* h = static_cast<char*>(host);
+      for (size_t q = 0; q < px; ++q) {
+        char* dst = h + q * o.C * esz;
+        if (which == DCNN_BUF_XT && !(fl[q] & 1)) memset(dst, 0, o.C * esz);
+        else memcpy(dst, ((which == DCNN_BUF_XA && (fl[q] & 2)) ? b1 : b0).data() + q * o.ld * esz, o.C * esz);
+      }
+      return DCNN_OK;
+    }
     if (esz) {
       nb = px * o.C * esz;
       if (bytes) *bytes = (int64_t)nb;
@@ -1226,7 +1417,7 @@ dcnn_status dcnn_debug_launch_times(dcnn_net* n, int32_t max, int32_t* op, int32
     if (k < max) {
       float e = 0.f;
       CUDA_TRY(cudaEventElapsedTime(&e, t.a, t.b));
-      if (op) op[k] = t.op;
+      if (op) op[k] = t.op < 0 ? t.op : n->uinv[t.op];
       if (cls) cls[k] = t.cls;
       if (ms) ms[k] = e;
     }

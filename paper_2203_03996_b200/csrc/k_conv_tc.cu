@@ -34,6 +34,17 @@
 //               tiles ("before loading any other data, we first check the update
 //               mask"); only active tiles enter the pipeline, through
 //               a ring of NI tile slots, so mask checks run ahead of the data loads.
+//
+// Single-pass truncation (p.xA2 != null).  The Eq. 4 decision of a pixel needs the max-norm
+// over ALL its output channels, but a thread holds up to 128 of them and cannot keep both
+// outcomes (x^A := s, delta := d  /  x^T := x^T + dx) of every channel until the norm is
+// known.  Instead every 32-channel slice writes BOTH outcomes speculatively, where neither
+// can be wrong: s goes to the pixel's other x^A buffer (x^A is double-buffered, bit 1 of the
+// pixel's state byte selects the current one), d to the delta rows (read only where the
+// mask is set), and x^T + dx over x^T in place (x^T is read only where bit 0 is set).
+// The decision then flips the pixel's state bits: updated -> other x^A buffer current, bit 0
+// cleared (x^T = 0, Eq. 6); truncated -> x^A buffer kept, bit 0 set (x^T += dx, Eq. 4).  One
+// global round trip per slice instead of a norm pass plus a recompute pass.
 #include "kernels.h"
 #include "tc.cuh"
 
@@ -135,7 +146,7 @@ __device__ __forceinline__ void unpack8<__half>(const uint4& u, float v[8]) {
   }
 }
 
-template <typename TC, int ACT>
+template <typename TC, int ACT, bool DBL>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant__ ConvTCParams p) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const TcSmem L = tc_layout(p);
@@ -588,7 +599,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       const long long row = pix * Cg + cb0 + c_lo;
       __half* dl = reinterpret_cast<__half*>(e.delta) + row;
       float* O = e.O ? e.O + row : nullptr;
-      TC* A = reinterpret_cast<TC*>(e.xA) + row;
+      const uint8_t fl = (act && p.tflag) ? p.tflag[pix] : (uint8_t)0;   // pixel state bits
+      TC* A = reinterpret_cast<TC*>((DBL && (fl & 2)) ? p.xA2 : e.xA) + row;   // current x^A row
       TC* Tt = reinterpret_cast<TC*>(e.xT) + row;
       const bool full_rows = vec && (C % 8) == 0;
       // ---- coalesced row access (fp16 rows) through this warp's staging areas SA / ST / SD
@@ -606,7 +618,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       // move the n16 16-B chunks of the rows of the pixels in pm between global rows
       // (base + pix * Cg) and a staging area; dir 0 = load into smem, 1 = store from smem
       // (dir 1: pixels in zm store zeros instead of the staged row)
-      auto stage_move = [&](unsigned char* area, __half* base, int n16, uint32_t pm, int dir, uint32_t zm = 0u) {
+      // (base1 / sel: pixels whose bit is set in sel use base1 instead of base)
+      auto stage_move = [&](unsigned char* area, __half* base, int n16, uint32_t pm, int dir, uint32_t zm = 0u,
+                            __half* base1 = nullptr, uint32_t sel = 0u) {
         const int lg = n16 > 2 ? 2 : n16 - 1, lp = 1 << lg;
         __syncwarp();
 #pragma unroll
@@ -614,7 +628,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           if (i >= lp) break;
           const int pl = (i << (5 - lg)) + (lane >> lg), c = lane & (lp - 1);
           if (c < n16 && ((pm >> pl) & 1u)) {
-            uint4* g = reinterpret_cast<uint4*>(base + (pixw + (long long)(pl >> 3) * p.Wo + (pl & 7)) * Cg + c * 8);
+            __half* b = ((sel >> pl) & 1u) ? base1 : base;
+            uint4* g = reinterpret_cast<uint4*>(b + (pixw + (long long)(pl >> 3) * p.Wo + (pl & 7)) * Cg + c * 8);
             uint4* sm = reinterpret_cast<uint4*>(area + pl * 80 + c * 16);
             if (dir) *g = ((zm >> pl) & 1u) ? make_uint4(0u, 0u, 0u, 0u) : *sm;
             else *sm = *g;
@@ -624,14 +639,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       };
       // fill SA / ST with the x^A / x^T rows of the pixels in pm: every global load of both
       // areas is issued before the first shared store (one round trip, not eight)
-      auto stage_fill2 = [&](const __half* baseA, const __half* baseT, int n16, uint32_t pm, uint32_t pmt) {
+      auto stage_fill2 = [&](const __half* baseA, const __half* baseT, int n16, uint32_t pm, uint32_t pmt,
+                             const __half* baseA1 = nullptr, uint32_t sel = 0u) {
         const int lg = n16 > 2 ? 2 : n16 - 1, lp = 1 << lg;
         uint4 va[4], vt[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int pl = (i << (5 - lg)) + (lane >> lg), c = lane & (lp - 1);
           const long long off = (pixw + (long long)(pl >> 3) * p.Wo + (pl & 7)) * Cg + c * 8;
-          if (i < lp && c < n16 && ((pm >> pl) & 1u)) va[i] = *reinterpret_cast<const uint4*>(baseA + off);
+          const __half* bA = ((sel >> pl) & 1u) ? baseA1 : baseA;
+          if (i < lp && c < n16 && ((pm >> pl) & 1u)) va[i] = *reinterpret_cast<const uint4*>(bA + off);
           if (i < lp && c < n16 && ((pmt >> pl) & 1u)) vt[i] = *reinterpret_cast<const uint4*>(baseT + off);
         }
         __syncwarp();
@@ -646,15 +663,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       const uint32_t actm = __ballot_sync(0xffffffffu, act);
       const long long chan0 = cb0 + c_lo;       // my first channel in the row
       __half* gA = reinterpret_cast<__half*>(e.xA) + chan0;
+      __half* gA2 = reinterpret_cast<__half*>(p.xA2) + chan0;
       __half* gT = reinterpret_cast<__half*>(e.xT) + chan0;
       __half* gD = reinterpret_cast<__half*>(e.delta) + chan0;
       auto n16_of = [&](int sl) { return C - sl >= 32 ? 4 : (C - sl) / 8; };
       const bool need_cache = trunc && !first;
+      const bool need_cache_w = need_cache;      // (warp-uniform: a tile is one stream)
       // pixels whose x^T may be non-zero (all active ones without the pending-residual flags)
-      const bool tpend = act && (p.tflag == nullptr || p.tflag[pix] != 0);
+      const bool tpend = act && (p.tflag == nullptr || (fl & 1));
       const uint32_t tm = __ballot_sync(0xffffffffu, tpend);
+      const bool dbl = DBL && COAL && coal && trunc;                    // single-pass truncation
+      const uint32_t selm = DBL ? __ballot_sync(0xffffffffu, (fl & 2) != 0) : 0u;   // pixels whose x^A is in xA2
       // ---- loads that do not depend on the accumulator: the first slice of the cache rows
-      if (need_cache && coal && actm && C > 0) stage_fill2(gA, gT, n16_of(0), actm, tm);
+      if (need_cache_w && coal && actm && C > 0) stage_fill2(gA, gT, n16_of(0), actm, tm, gA2, selm);
       if (act && O && !first)
         for (int c = 0; c < C; c += 32) prefetch_l2(O + c);
       // the later 32-channel slices of the cache rows: into L2 while the MMAs run, so the
@@ -696,13 +717,81 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         }
       };
       bool upd = act;
+      // the pixel's max-norm over its channels: the two halves of this CTA, and every CTA of
+      // the cluster (DSMEM exchange)
+      auto norm_combine = [&](float mx) -> float {
+        const int xb = u & 1;
+        pm2[xb * 256 + half * 128 + m] = mx;
+        tc::named_bar_sync(2, 256);
+        mx = fmaxf(pm2[xb * 256 + m], pm2[xb * 256 + 128 + m]);
+        if (nsplit > 1) {
+          if (half == 0) pmax[xb * 128 + m] = mx;
+          tc::named_bar_sync(2, 256);
+          if (tid == 0) {
+            const uint32_t local = tc::smem_u32(&xch[xb]);
+            for (int r = 0; r < nsplit; ++r) tc::mbar_arrive_remote(tc::mapa(local, (uint32_t)r));
+          }
+          tc::mbar_wait_cluster(&xch[xb], (u >> 1) & 1);
+          const uint32_t mine = tc::smem_u32(&pmax[xb * 128 + m]);
+          for (int r = 0; r < nsplit; ++r) mx = fmaxf(mx, tc::ld_dsmem_f32(tc::mapa(mine, (uint32_t)r)));
+        }
+        return mx;
+      };
+      if (dbl) {
+        // ---- single pass (see the header): per 32-channel slice, both outcomes written at once
+        const bool known_upd = first || eps < 0.f;   // this pixel surely updates: x^T := 0 by bit 0
+        const uint32_t tw = known_upd ? 0u : actm;   // x^T + dx rows to write
+        float mx = 0.f;
+#pragma unroll 1
+        for (int sl = 0; sl < C; sl += 32) {
+          const int n16 = n16_of(sl);
+          if (sl > 0 && need_cache_w && actm) stage_fill2(gA + sl, gT + sl, n16, actm, tm, gA2 + sl, selm);
+#pragma unroll 1
+          for (int c0 = sl; c0 < C && c0 < sl + 32; c0 += 8) {
+            float z[8], a[8], t[8];
+            chunk_in(c0, z, a, t);
+            if (act) {
+              float o[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const float prev = first ? 0.f : act_tc<ACT>(a[k], e.act_param);
+                const float sv = a[k] + t[k] + z[k];
+                const float d = act_tc<ACT>(sv, e.act_param) - prev;
+                if (c0 + k < C) mx = fmaxf(mx, fabsf(d));
+                o[k] = d;
+                a[k] = sv;                     // x^A if updated (Eq. 6)
+                t[k] += z[k];                  // x^T if truncated (Eq. 4)
+              }
+              const int off = lane * 80 + (c0 & 31) * 2;
+              *reinterpret_cast<uint4*>(SD + off) =
+                  make_uint4(pack_h2(o[0], o[1]), pack_h2(o[2], o[3]), pack_h2(o[4], o[5]), pack_h2(o[6], o[7]));
+              *reinterpret_cast<uint4*>(SA + off) =
+                  make_uint4(pack_h2(a[0], a[1]), pack_h2(a[2], a[3]), pack_h2(a[4], a[5]), pack_h2(a[6], a[7]));
+              if (!known_upd)
+                *reinterpret_cast<uint4*>(ST + off) =
+                    make_uint4(pack_h2(t[0], t[1]), pack_h2(t[2], t[3]), pack_h2(t[4], t[5]), pack_h2(t[6], t[7]));
+            }
+          }
+          TCTR(tid == 0 && u == 0 && sl == 0, 19);
+          if (actm) {
+            stage_move(SA, gA2 + sl, n16, actm, 1, 0u, gA + sl, selm);   // s -> the other x^A buffer
+            stage_move(SD, gD + sl, n16, actm, 1);
+            if (tw) stage_move(ST, gT + sl, n16, tw, 1);
+          }
+          TCTR(tid == 0 && u == 0 && sl == 0, 20);
+        }
+        TCTR(tid == 0 && u == 0, 15);
+        mx = norm_combine(mx);
+        TCTR(tid == 0 && u == 0, 16);
+        upd = act && (first || eps < 0.f || mx > eps);
+      }
       // <= 32 channels per thread with coalesced rows: one pass (pass 1 stages both outcomes)
       const bool single = trunc && coal && C > 0 && C <= 32;
-      if (trunc) {
+      if (trunc && !dbl) {
         float mx = 0.f;
 #pragma unroll 1
         for (int c0 = 0; c0 < C; c0 += 8) {
-          if (coal && need_cache && actm && c0 > 0 && (c0 & 31) == 0)     // next slice
+          if (coal && need_cache_w && actm && c0 > 0 && (c0 & 31) == 0)     // next slice
             stage_fill2(gA + c0, gT + c0, n16_of(c0), actm, tm);
           float z[8], a[8], t[8];
           chunk_in(c0, z, a, t);
@@ -730,23 +819,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           }
         }
         TCTR(tid == 0 && u == 0, 15);
-        // max-norm over the pixel's channels: the two halves of this CTA ...
-        const int xb = u & 1;
-        pm2[xb * 256 + half * 128 + m] = mx;
-        tc::named_bar_sync(2, 256);
-        mx = fmaxf(pm2[xb * 256 + m], pm2[xb * 256 + 128 + m]);
-        if (nsplit > 1) {
-          // ... and every CTA of the cluster (DSMEM exchange)
-          if (half == 0) pmax[xb * 128 + m] = mx;
-          tc::named_bar_sync(2, 256);
-          if (tid == 0) {
-            const uint32_t local = tc::smem_u32(&xch[xb]);
-            for (int r = 0; r < nsplit; ++r) tc::mbar_arrive_remote(tc::mapa(local, (uint32_t)r));
-          }
-          tc::mbar_wait_cluster(&xch[xb], (u >> 1) & 1);
-          const uint32_t mine = tc::smem_u32(&pmax[xb * 128 + m]);
-          for (int r = 0; r < nsplit; ++r) mx = fmaxf(mx, tc::ld_dsmem_f32(tc::mapa(mine, (uint32_t)r)));
-        }
+        mx = norm_combine(mx);
         upd = act && (first || eps < 0.f || mx > eps);
       }
       TCTR(tid == 0 && u == 0, 16);
@@ -754,9 +827,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       // ---- pass 2: results of each 32-channel slice staged in SA (x^A), ST (x^T), SD (delta),
       // then flushed with coalesced stores
 #pragma unroll 1
-      for (int c0 = single ? (C - 1) & ~7 : 0; c0 < C; c0 += 8) {
+      for (int c0 = dbl ? C : single ? (C - 1) & ~7 : 0; c0 < C; c0 += 8) {
         if (single) goto flush;                  // results already staged by pass 1
-        if (coal && need_cache && actm && (c0 & 31) == 0 && (c0 > 0 || C > 32))     // reload the slice
+        if (coal && need_cache_w && actm && (c0 & 31) == 0 && (c0 > 0 || C > 32))     // reload the slice
           stage_fill2(gA + c0, gT + c0, n16_of(c0), actm, tm);
         float z[8], a[8], t[8], o[8];
         chunk_in(c0, z, a, t);
@@ -848,7 +921,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       if (inb && rank == 0 && half == 0) e.mask[pix] = upd ? 1 : 0;   // final mask of every tile pixel
       // pending-residual flag: written by one thread per pixel after every CTA of the cluster
       // and both halves have read it (they all passed the max-norm exchange)
-      if (trunc && p.tflag && act && rank == 0 && half == 0 && upd == tpend) p.tflag[pix] = upd ? 0 : 1;
+      if (dbl) {
+        // updated: the other x^A buffer becomes current, x^T = 0; truncated: x^T pending
+        if (act && rank == 0 && half == 0) p.tflag[pix] = upd ? (uint8_t)((fl & 2) ^ 2) : (uint8_t)((fl & 2) | 1);
+      } else if (trunc && p.tflag && act && rank == 0 && half == 0 && upd == tpend) {
+        p.tflag[pix] = upd ? 0 : 1;
+      }
       nact += (upd && rank == 0 && half == 0) ? 1 : 0;
       TCTR(tid == 0 && u == 0, 12);
       tc::tc_fence_before();
@@ -878,9 +956,14 @@ static cudaError_t tc_attr() {
   cudaError_t err = cudaSuccess;
   for (int a = 0; a <= ACT_SIGMOID; ++a)
     act_dispatch(a, [&](auto A) {
-      cudaError_t e = cudaFuncSetAttribute(k_conv_tc<TC, decltype(A)::value>,
+      cudaError_t e = cudaFuncSetAttribute(k_conv_tc<TC, decltype(A)::value, false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
       if (e != cudaSuccess) err = e;
+      if (std::is_same<TC, __half>::value) {
+        e = cudaFuncSetAttribute(k_conv_tc<TC, decltype(A)::value, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+        if (e != cudaSuccess) err = e;
+      }
     });
   return err;
 }
@@ -899,8 +982,9 @@ void launch_conv_tc(const ConvTCParams& p, int cache32, int grid, cudaStream_t s
     const size_t smem = conv_tc_smem(p) > 116 * 1024 ? conv_tc_smem(p) : 116 * 1024;
     // nsplit > 1: launched as clusters of nsplit CTAs (the kernel only uses cluster
     // barriers / DSMEM in that case)
-    if (cache32) launch_k(k_conv_tc<float, ACT>, dim3(grid), dim3(TC_THREADS), smem, st, p.nsplit, p);
-    else launch_k(k_conv_tc<__half, ACT>, dim3(grid), dim3(TC_THREADS), smem, st, p.nsplit, p);
+    if (cache32) launch_k(k_conv_tc<float, ACT, false>, dim3(grid), dim3(TC_THREADS), smem, st, p.nsplit, p);
+    else if (p.xA2) launch_k(k_conv_tc<__half, ACT, true>, dim3(grid), dim3(TC_THREADS), smem, st, p.nsplit, p);
+    else launch_k(k_conv_tc<__half, ACT, false>, dim3(grid), dim3(TC_THREADS), smem, st, p.nsplit, p);
   });
 }
 

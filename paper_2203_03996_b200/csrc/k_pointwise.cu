@@ -17,7 +17,22 @@
 namespace dcnn {
 
 enum Kind { K_CONV = 0, K_ACT = 1, K_MAXPOOL = 2, K_AVGPOOL = 3, K_UP = 4, K_ADD = 5, K_CONCAT = 6,
-            K_AFFINE = 7 };
+            K_AFFINE = 7, K_UPBIL = 8, K_ZINS = OP_ZERO_INSERT, K_DW = KIND_DEPTHWISE };
+
+// x f bilinear upsampling, align_corners = false: output coordinate o reads source i0 with weight
+// 1 - l and i1 = min(i0 + 1, n - 1) with weight l, where (o + 0.5) / f - 0.5 = (2o + 1 - f) / 2f,
+// clamped at 0, is split into i0 + l with integer arithmetic (the index is exact)
+__device__ __forceinline__ void bil_taps(int o, int f, int n, int& i0, int& i1, float& l) {
+  const int num = 2 * o + 1 - f;
+  if (num <= 0) {
+    i0 = 0;
+    l = 0.f;
+  } else {
+    i0 = num / (2 * f);
+    l = (float)(num - i0 * 2 * f) / (float)(2 * f);
+  }
+  i1 = min(i0 + 1, n - 1);
+}
 
 template <int KIND>
 __device__ __forceinline__ bool pw_mask(const PwParams& p, long long pix, int s, bool first) {
@@ -31,6 +46,30 @@ __device__ __forceinline__ bool pw_mask(const PwParams& p, long long pix, int s,
   const long long HWo = (long long)p.H * p.W;
   const int y = (int)((pix % HWo) / p.W), x = (int)(pix % p.W);
   if (KIND == K_UP) return p.min[0][((long long)s * p.Hi + y / p.up) * p.Wi + x / p.up] != 0;
+  if (KIND == K_ZINS)                 // inserted zeros are inactive
+    return y % p.up == 0 && x % p.up == 0 && p.min[0][((long long)s * p.Hi + y / p.up) * p.Wi + x / p.up] != 0;
+  if (KIND == K_DW) {                 // receptive-field OR (Z7), padding inactive
+    const uint8_t* mi = p.min[0] + (long long)s * p.Hi * p.Wi;
+    for (int ky = 0; ky < p.k; ++ky) {
+      const int iy = y * p.stride - p.pad + ky * p.dil;
+      if (iy < 0 || iy >= p.Hi) continue;
+      for (int kx = 0; kx < p.k; ++kx) {
+        const int ix = x * p.stride - p.pad + kx * p.dil;
+        if (ix >= 0 && ix < p.Wi && mi[iy * p.Wi + ix]) return true;
+      }
+    }
+    return false;
+  }
+  if (KIND == K_UPBIL) {              // any source with a non-zero weight active
+    int y0, y1, x0, x1;
+    float ly, lx;
+    bil_taps(y, p.up, p.Hi, y0, y1, ly);
+    bil_taps(x, p.up, p.Wi, x0, x1, lx);
+    const uint8_t* mi = p.min[0] + (long long)s * p.Hi * p.Wi;
+    bool m = mi[y0 * p.Wi + x0] || (lx > 0.f && mi[y0 * p.Wi + x1]);
+    if (ly > 0.f) m = m || mi[y1 * p.Wi + x0] || (lx > 0.f && mi[y1 * p.Wi + x1]);
+    return m;
+  }
   // pools: window OR (padding inactive)
   const uint8_t* mi = p.min[0] + (long long)s * p.Hi * p.Wi;
   for (int ky = 0; ky < p.k; ++ky) {
@@ -80,6 +119,65 @@ __device__ __forceinline__ void pw_chunk(const PwParams& p, long long pix, int s
     const int y = (int)((pix % HWo) / p.W), x = (int)(pix % p.W);
     const long long src = ((long long)s * p.Hi + y / p.up) * p.Wi + x / p.up;
     ld8(in0 + src * C + 8 * j, z);
+  } else if (KIND == K_DW) {
+    // depthwise delta conv, per-pixel sparse: each input pixel's update flag
+    // is checked before its value is loaded, and load + multiply are fused per tap
+    const long long HWo = (long long)p.H * p.W;
+    const int y = (int)((pix % HWo) / p.W), x = (int)(pix % p.W);
+    const uint8_t* mi = p.min[0] + (long long)s * p.Hi * p.Wi;
+    const long long base = (long long)s * p.Hi * p.Wi;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) z[k] = first ? p.bdw[8 * j + k] : 0.f;    // bias on frame 0 (Z6)
+    for (int ky = 0; ky < p.k; ++ky) {
+      const int iy = y * p.stride - p.pad + ky * p.dil;
+      if (iy < 0 || iy >= p.Hi) continue;
+      for (int kx = 0; kx < p.k; ++kx) {
+        const int ix = x * p.stride - p.pad + kx * p.dil;
+        if (ix < 0 || ix >= p.Wi || !(first || mi[iy * p.Wi + ix])) continue;
+        float v[8];
+        ld8(in0 + (base + (long long)iy * p.Wi + ix) * C + 8 * j, v);
+        const float4* w = reinterpret_cast<const float4*>(p.wdw + (long long)(ky * p.k + kx) * C + 8 * j);
+        const float4 w0 = w[0], w1 = w[1];
+        z[0] = fmaf(w0.x, v[0], z[0]); z[1] = fmaf(w0.y, v[1], z[1]);
+        z[2] = fmaf(w0.z, v[2], z[2]); z[3] = fmaf(w0.w, v[3], z[3]);
+        z[4] = fmaf(w1.x, v[4], z[4]); z[5] = fmaf(w1.y, v[5], z[5]);
+        z[6] = fmaf(w1.z, v[6], z[6]); z[7] = fmaf(w1.w, v[7], z[7]);
+      }
+    }
+  } else if (KIND == K_ZINS) {
+    const long long HWo = (long long)p.H * p.W;
+    const int y = (int)((pix % HWo) / p.W), x = (int)(pix % p.W);
+    if (y % p.up == 0 && x % p.up == 0) {
+      ld8(in0 + (((long long)s * p.Hi + y / p.up) * p.Wi + x / p.up) * C + 8 * j, z);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) z[k] = 0.f;
+    }
+  } else if (KIND == K_UPBIL) {
+    const long long HWo = (long long)p.H * p.W;
+    const int y = (int)((pix % HWo) / p.W), x = (int)(pix % p.W);
+    int y0, y1, x0, x1;
+    float ly, lx;
+    bil_taps(y, p.up, p.Hi, y0, y1, ly);
+    bil_taps(x, p.up, p.Wi, x0, x1, lx);
+    const long long base = (long long)s * p.Hi * p.Wi;
+    const int ys[2] = {y0, y1}, xs[2] = {x0, x1};
+    const float wy[2] = {1.f - ly, ly}, wx[2] = {1.f - lx, lx};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) z[k] = 0.f;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const long long q = base + (long long)ys[a] * p.Wi + xs[b];
+        const float w = wy[a] * wx[b];
+        if (w > 0.f && (first || p.min[0][q])) {             // inactive sources contribute 0
+          float v[8];
+          ld8(in0 + q * C + 8 * j, v);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) z[k] += w * v[k];
+        }
+      }
   } else {  // pools
     const long long HWo = (long long)p.H * p.W;
     const int y = (int)((pix % HWo) / p.W), x = (int)(pix % p.W);
@@ -154,6 +252,40 @@ __device__ __forceinline__ float pw_scalar(const PwParams& p, long long pix, int
     const long long src = ((long long)s * p.Hi + y / p.up) * p.Wi + x / p.up;
     return ld(in0 + src * C + c);
   }
+  if (KIND == K_DW) {
+    const uint8_t* mi = p.min[0] + (long long)s * p.Hi * p.Wi;
+    float z = first ? p.bdw[c] : 0.f;
+    for (int ky = 0; ky < p.k; ++ky) {
+      const int iy = y * p.stride - p.pad + ky * p.dil;
+      if (iy < 0 || iy >= p.Hi) continue;
+      for (int kx = 0; kx < p.k; ++kx) {
+        const int ix = x * p.stride - p.pad + kx * p.dil;
+        if (ix < 0 || ix >= p.Wi || !(first || mi[iy * p.Wi + ix])) continue;
+        z = fmaf(p.wdw[(ky * p.k + kx) * C + c], ld(in0 + (((long long)s * p.Hi + iy) * p.Wi + ix) * C + c), z);
+      }
+    }
+    return z;
+  }
+  if (KIND == K_ZINS)
+    return (y % p.up == 0 && x % p.up == 0)
+               ? ld(in0 + (((long long)s * p.Hi + y / p.up) * p.Wi + x / p.up) * C + c) : 0.f;
+  if (KIND == K_UPBIL) {
+    int y0, y1, x0, x1;
+    float ly, lx;
+    bil_taps(y, p.up, p.Hi, y0, y1, ly);
+    bil_taps(x, p.up, p.Wi, x0, x1, lx);
+    const long long base = (long long)s * p.Hi * p.Wi;
+    const int ys[2] = {y0, y1}, xs[2] = {x0, x1};
+    const float wy[2] = {1.f - ly, ly}, wx[2] = {1.f - lx, lx};
+    float z = 0.f;
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        const long long q = base + (long long)ys[a] * p.Wi + xs[b];
+        const float w = wy[a] * wx[b];
+        if (w > 0.f && (first || p.min[0][q])) z += w * ld(in0 + q * C + c);
+      }
+    return z;
+  }
   const uint8_t* mi = p.min[0] + (long long)s * p.Hi * p.Wi;
   const TC* A = reinterpret_cast<const TC*>(p.poolA);
   const long long base = (long long)s * p.Hi * p.Wi;
@@ -191,7 +323,7 @@ __global__ void __launch_bounds__(256) k_pointwise(PwParams p) {
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   const int G = p.vec ? p.G : 32;
   const int PPW = 32 / G, gi = lane / G, gl = lane % G;
-  unsigned nact = 0;
+  unsigned nact = 0, nmc = 0;
   // warp w finishes pixels [w*PPW, w*PPW+PPW): one group of G lanes per pixel
   for (long long base = gw * PPW; base < npix; base += nw * PPW) {
     const long long q = base + gi;
@@ -215,9 +347,14 @@ __global__ void __launch_bounds__(256) k_pointwise(PwParams p) {
                                     [&](int c) { return pw_scalar<T, TC, KIND>(p, q, s, first, mk, c); });
     }
     if (valid && gl == 0 && up) ++nact;
+    if (KIND == K_DW && valid && gl == 0) ++nmc;
   }
   const unsigned tot = (unsigned)warp_sum((int)nact);
   warp_count_flush(p.ep.n_active, lane, tot);
+  if (KIND == K_DW) {
+    const unsigned m = (unsigned)warp_sum((int)nmc);
+    if (lane == 0 && m) atomicAdd(p.mconv, (unsigned long long)m);
+  }
 }
 
 // max-pool accumulated input update, after the pool outputs were computed from
@@ -256,9 +393,14 @@ static void pw_dispatch(const PwParams& p, cudaStream_t st) {
     case K_ADD:
       act_dispatch(p.ep.act, [&](auto a) { launch_k(k_pointwise<T, TC, K_ADD, decltype(a)::value>, dim3(grid), dim3(256), 0, st, 1, p); });
       break;
+    case K_DW:
+      act_dispatch(p.ep.act, [&](auto a) { launch_k(k_pointwise<T, TC, K_DW, decltype(a)::value>, dim3(grid), dim3(256), 0, st, 1, p); });
+      break;
     case K_MAXPOOL: launch_k(k_pointwise<T, TC, K_MAXPOOL, ACT_NONE>, dim3(grid), dim3(256), 0, st, 1, p); break;
     case K_AVGPOOL: launch_k(k_pointwise<T, TC, K_AVGPOOL, ACT_NONE>, dim3(grid), dim3(256), 0, st, 1, p); break;
     case K_UP: launch_k(k_pointwise<T, TC, K_UP, ACT_NONE>, dim3(grid), dim3(256), 0, st, 1, p); break;
+    case K_UPBIL: launch_k(k_pointwise<T, TC, K_UPBIL, ACT_NONE>, dim3(grid), dim3(256), 0, st, 1, p); break;
+    case K_ZINS: launch_k(k_pointwise<T, TC, K_ZINS, ACT_NONE>, dim3(grid), dim3(256), 0, st, 1, p); break;
     case K_CONCAT: launch_k(k_pointwise<T, TC, K_CONCAT, ACT_NONE>, dim3(grid), dim3(256), 0, st, 1, p); break;
     case K_AFFINE: launch_k(k_pointwise<T, TC, K_AFFINE, ACT_NONE>, dim3(grid), dim3(256), 0, st, 1, p); break;
   }

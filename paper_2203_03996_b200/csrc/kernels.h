@@ -114,8 +114,10 @@ struct ConvTCParams {
   int fused;                    // 1: iterate all tiles, decide activity in-kernel (no a2 launch)
   int ntiles;                   // S*nty*ntx (fused mode)
   unsigned long long* tstats;   // fused mode: [.., tiles_total, skip, sparse, dense, m_conv px]
-  uint8_t* tflag;               // [S,Ho,Wo] x^T != 0 ("pending residual") or null: x^T is then
-                                // read only where flagged and written only when it changes
+  uint8_t* tflag;               // [S,Ho,Wo] per-pixel state bits or null.  bit 0: x^T != 0
+                                // ("pending residual"): x^T is read only where it is set.
+                                // bit 1 (xA2 != null): x^A of the pixel lives in xA2, else in ep.xA
+  void* xA2;                    // second x^A buffer (single-pass epilogue, see k_conv_tc.cu) or null
   const __half* delta_in;
   const uint8_t* mask_in;
   const __half* wtc;            // [nsplit][ncb*kh*kw][BK/8][Ns][8] fp16 (smem image of each step)
@@ -127,6 +129,13 @@ size_t conv_tc_smem(const ConvTCParams& p);
 cudaError_t conv_tc_init();
 void launch_conv_tc(const ConvTCParams& p, int cache32, int grid, cudaStream_t st);
 cudaError_t conv_tc_read_trace(unsigned long long* host);   // debug timeline (dbg & 4)
+
+// internal op kind (not in dcnn.h): zero-insertion upsampling of a delta and its mask, the first
+// half of a lowered DCNN_OP_CONV_TRANSPOSE (dcnn_create_net)
+constexpr int OP_ZERO_INSERT = 16;
+// internal kernel kind of a depthwise delta conv (a DCNN_OP_CONV with groups == C_in == C_out):
+// the per-pixel sparse CUDA-core kernel of PAPER.md:661-667 (S1.2) on the pointwise skeleton
+constexpr int KIND_DEPTHWISE = 17;
 
 // ---------------------------------------------------------------- a6/a7 pointwise ops
 struct PwParams {
@@ -140,6 +149,10 @@ struct PwParams {
   int k, stride, pad, up;       // pool window / upsample factor
   const float* scale; const float* shift;  // affine
   void* poolA;                  // maxpool accumulated input [S,Hi,Wi,C] (cache type)
+  int dil;                      // depthwise conv: dilation
+  const float* wdw;             // depthwise conv: weights [k*k][C] fp32 (values of the storage dtype)
+  const float* bdw;             // depthwise conv: bias [C] (first frame only)
+  unsigned long long* mconv;    // depthwise conv: receptive-field-active output pixels (stats)
   int vec, G;                   // 8-channel chunk path, lanes per pixel
   Epi ep;
 };

@@ -21,7 +21,7 @@ from typing import List, Optional
 import numpy as np
 
 ACTS = ("none", "relu", "silu", "relu6", "leaky", "sigmoid")
-OPS = ("conv", "act", "maxpool", "avgpool", "up", "add", "concat", "affine")
+OPS = ("conv", "act", "maxpool", "avgpool", "up", "add", "concat", "affine", "upbilinear", "convtranspose")
 
 
 @dataclasses.dataclass
@@ -131,9 +131,24 @@ class _Builder:
             C += self.shape[s][2]
         return self._add(Layer("concat", list(srcs), name=name), (H, W, C))
 
-    def up(self, src, f, name=""):
+    def conv_transpose(self, src, c_out, k, stride=2, pad=1, act="none", gain=None, name=""):
+        """Transposed conv (weights [C_out, k, k, C_in]; see oracle.conv_transpose2d); output
+        (H - 1) * stride - 2 * pad + k."""
         H, W, C = self.shape[src]
-        return self._add(Layer("up", [src], up=f, name=name), (H * f, W * f, C))
+        if gain is None:
+            gain = {"relu": np.sqrt(2.0), "silu": 1.7, "none": 1.0}.get(act, 1.0)
+        fan_in = k * k * C / (stride * stride)            # inputs reaching one output pixel
+        w = self.rng.standard_normal((c_out, k, k, C)) * (gain / np.sqrt(fan_in))
+        b = self.rng.uniform(-0.1, 0.1, size=c_out)
+        Ho, Wo = (H - 1) * stride - 2 * pad + k, (W - 1) * stride - 2 * pad + k
+        return self._add(Layer("convtranspose", [src], c_out=c_out, kh=k, kw=k, stride=stride, pad=pad,
+                               act=act, weight=w.astype(np.float32), bias=b.astype(np.float32), name=name),
+                         (Ho, Wo, c_out))
+
+    def up(self, src, f, name="", mode="nearest"):
+        H, W, C = self.shape[src]
+        op = "up" if mode == "nearest" else "upbilinear"
+        return self._add(Layer(op, [src], up=f, name=name), (H * f, W * f, C))
 
     def maxpool(self, src, k, stride, pad, name=""):
         H, W, C = self.shape[src]
@@ -194,8 +209,18 @@ def lsuv(net: Net, calib_hw=None, seed: int = 0) -> Net:
                 y = F.max_pool2d(xs[0], L.kh, L.stride, L.pad)
             elif L.op == "avgpool":
                 y = F.avg_pool2d(xs[0], L.kh, L.stride, L.pad)
+            elif L.op == "convtranspose":
+                w = torch.from_numpy(L.weight.astype(np.float64)).permute(3, 0, 1, 2)
+                z = F.conv_transpose2d(xs[0], w, None, stride=L.stride, padding=L.pad)
+                r = float(z.pow(2).mean().sqrt())
+                if r > 0:
+                    L.weight = (L.weight.astype(np.float64) / r).astype(np.float32)
+                z = z / max(r, 1e-30) + torch.from_numpy(L.bias.astype(np.float64)).view(1, -1, 1, 1)
+                y = acts[L.act](z)
             elif L.op == "up":
                 y = F.interpolate(xs[0], scale_factor=L.up, mode="nearest")
+            elif L.op == "upbilinear":
+                y = F.interpolate(xs[0], scale_factor=L.up, mode="bilinear", align_corners=False)
             elif L.op == "add":
                 y = acts[L.act](sum(xs))
             elif L.op == "concat":
@@ -442,7 +467,11 @@ def random_net(seed: int, H: int = 24, W: int = 20, C_in: int = 4, n_layers: int
         elif kind == "avgpool" and min(Hs, Ws) >= 6:
             cur = b.avgpool(src, 2, 2, 0, name=f"ap{li}")
         elif kind == "up" and max(Hs, Ws) <= 32:
-            cur = b.up(src, 2, name=f"u{li}")
+            # (no extra draw: the graphs of earlier seeds keep their structure)
+            if li % 3 == 1:
+                cur = b.conv_transpose(src, 8, 4, 2, 1, act="relu", name=f"ct{li}")
+            else:
+                cur = b.up(src, 2, name=f"u{li}", mode="bilinear" if li % 2 == 0 else "nearest")
         elif kind == "add":
             cands = [a for a in avail if b.shape[a] == b.shape[src] and a != src]
             if cands:
@@ -462,6 +491,126 @@ def random_net(seed: int, H: int = 24, W: int = 20, C_in: int = 4, n_layers: int
     b.net.outputs = [avail[-1]] + ([avail[-2]] if len(avail) > 2 and rng.random() < 0.5 else [])
     b.net.input_eps = eps
     b.net.input_dilation = int(rng.choice([0, 0, 1, 2]))
+    b.net.set_inner_eps(eps)
+    return b.net
+
+
+def pose_resnet_head(H: int = 128, W: int = 96, C: int = 64, eps: float = 0.05, seed: int = 9,
+                     dtype: str = "f16", bilinear: bool = False, n_joints: int = 17) -> Net:
+    """NEXT-4: a Pose-ResNet-style net (the paper's third network): a strided conv
+    backbone to H/16, then three 4x4 stride-2 transposed convs (+ReLU) back to H/2, and a 1x1
+    head to the joint heatmaps.  bilinear=True replaces the middle transposed conv by a x2
+    bilinear upsampling followed by a 3x3 conv."""
+    b = _Builder("pose_resnet", H, W, 3, seed, dtype)
+    x = b.conv(-1, 32, 3, stride=2, act="relu")
+    x = b.conv(x, C, 3, stride=2, act="relu")
+    x = b.conv(x, 2 * C, 3, stride=2, act="relu")
+    x = b.conv(x, 2 * C, 3, stride=2, act="relu")
+    x = b.conv_transpose(x, C, 4, 2, 1, act="relu", name="deconv1")
+    if bilinear:
+        x = b.up(x, 2, name="up2", mode="bilinear")
+        x = b.conv(x, C, 3, act="relu", name="conv_up2")
+    else:
+        x = b.conv_transpose(x, C, 4, 2, 1, act="relu", name="deconv2")
+    x = b.conv_transpose(x, C, 4, 2, 1, act="relu", name="deconv3")
+    h = b.conv(x, n_joints, 1, act="none", name="heatmaps")
+    b.net.outputs = [h]
+    lsuv(b.net, None, seed)
+    b.net.input_eps = eps
+    b.net.input_dilation = 0
+    b.net.set_inner_eps(eps)
+    return b.net
+
+
+def efficientdet_lite0(H: int = 384, W: int = 384, eps: float = 0.05, input_eps: float = 0.5,
+                       input_dilation: int = 7, seed: int = 11, dtype: str = "f16", n_classes: int = 20,
+                       n_anchors: int = 9, bifpn_ch: int = 64, bifpn_layers: int = 3,
+                       head_repeats: int = 3) -> Net:
+    """NEXT-1: EfficientDet-Lite0 (the paper's detector family, with the Lite
+    backbone, i.e. EfficientNet-B0 blocks without squeeze-and-excitation and with ReLU6):
+    stem 3x3 s2 -> 16 MBConv blocks (1x1 expand + ReLU6, depthwise k x k + ReLU6, 1x1 project,
+    residual add), B0 stage table (t, c, n, s, k) = (1,16,1,1,3) (6,24,2,2,3) (6,40,2,2,5)
+    (6,80,3,2,3) (6,112,3,1,5) (6,192,4,2,5) (6,320,1,1,3); BiFPN over P3-P7 (64 channels,
+    3 layers, fast normalised fusion = constant per-input scales + add + ReLU6, then a
+    depthwise-separable conv; nearest x2 up, 3x3 s2 max-pool down); class / box heads shared
+    over the levels (3 separable convs + ReLU6, then separable convs to anchors x classes and
+    anchors x 4).  n_classes is reduced from COCO's 90 for the synthetic workload; the input side
+    must be a multiple of 128 (P7 = H / 128; Lite0's own 320 needs resize-to-size fusion)."""
+    b = _Builder("efficientdet_lite0", H, W, 3, seed, dtype)
+    damp = 0.5
+    x = b.conv(-1, 32, 3, stride=2, act="relu6", name="stem")
+    stages = [(1, 16, 1, 1, 3), (6, 24, 2, 2, 3), (6, 40, 2, 2, 5), (6, 80, 3, 2, 3),
+              (6, 112, 3, 1, 5), (6, 192, 4, 2, 5), (6, 320, 1, 1, 3)]
+    cin, feats = 32, {}
+    for si, (t, c, n, s, k) in enumerate(stages):
+        for r in range(n):
+            stride = s if r == 0 else 1
+            res = stride == 1 and cin == c
+            h = x if t == 1 else b.conv(x, cin * t, 1, act="relu6", name=f"b{si}.{r}.expand")
+            h = b.conv(h, cin * t, k, stride=stride, groups=cin * t, act="relu6", name=f"b{si}.{r}.dw")
+            h = b.conv(h, c, 1, act="none", gain=damp if res else None, name=f"b{si}.{r}.project")
+            x = b.add([x, h], name=f"b{si}.{r}.add") if res else h
+            cin = c
+        if si in (2, 4, 6):
+            feats[{2: 3, 4: 4, 6: 5}[si]] = x
+    F = bifpn_ch
+
+    def down(v, name):
+        return b.maxpool(v, 3, 2, 1, name=name)
+
+    def sepconv(v, c_out, act, name):
+        v = b.conv(v, b.shape[v][2], 3, groups=b.shape[v][2], act="none", name=name + ".dw")
+        return b.conv(v, c_out, 1, act=act, name=name + ".pw")
+
+    def fuse(srcs, name):
+        w = 1.0 / len(srcs)                   # fast normalised fusion with equal weights
+        parts = []
+        for j, v in enumerate(srcs):
+            a = b.affine(v, name=f"{name}.w{j}")
+            L = b.net.layers[a]
+            L.scale = np.full_like(L.scale, w)
+            L.shift = np.zeros_like(L.shift)
+            parts.append(a)
+        return sepconv(b.add(parts, act="relu6", name=name + ".sum"), F, "none", name)
+
+    P = {lv: b.conv(feats[lv], F, 1, act="none", name=f"lat{lv}") for lv in (3, 4, 5)}
+    P[6] = down(P[5], "p6")
+    P[7] = down(P[6], "p7")
+    for li in range(bifpn_layers):
+        td = {7: P[7]}
+        for lv in (6, 5, 4):
+            td[lv] = fuse([P[lv], b.up(td[lv + 1], 2, name=f"bf{li}.up{lv}")], f"bf{li}.td{lv}")
+        out = {3: fuse([P[3], b.up(td[4], 2, name=f"bf{li}.up3")], f"bf{li}.out3")}
+        for lv in (4, 5, 6):
+            out[lv] = fuse([P[lv], td[lv], down(out[lv - 1], f"bf{li}.down{lv}")], f"bf{li}.out{lv}")
+        out[7] = fuse([P[7], down(out[6], f"bf{li}.down7")], f"bf{li}.out7")
+        P = out
+    outputs = []
+    shared = {}
+    for lv in (3, 4, 5, 6, 7):
+        for head, c_last in (("cls", n_anchors * n_classes), ("box", n_anchors * 4)):
+            v = P[lv]
+            for r in range(head_repeats):
+                v = sepconv(v, F, "relu6", f"{head}{r}.p{lv}")
+            v = sepconv(v, c_last, "none", f"{head}_out.p{lv}")
+            outputs.append(v)
+    # heads share their weights over the levels (as in EfficientDet)
+    for i, L in enumerate(b.net.layers):
+        if L.op == "conv" and (L.name.startswith("cls") or L.name.startswith("box")):
+            key = L.name.rsplit(".p", 1)[0] + L.name[L.name.rindex("."):]
+            if key in shared:
+                L.weight, L.bias = shared[key]
+    b.net.outputs = outputs
+    lsuv(b.net, None, seed)
+    for L in b.net.layers:                    # re-share after the per-layer rescaling
+        if L.op == "conv" and (L.name.startswith("cls") or L.name.startswith("box")):
+            key = L.name.rsplit(".p", 1)[0] + L.name[L.name.rindex("."):]
+            if key in shared:
+                L.weight, L.bias = shared[key]
+            else:
+                shared[key] = (L.weight, L.bias)
+    b.net.input_eps = input_eps
+    b.net.input_dilation = input_dilation
     b.net.set_inner_eps(eps)
     return b.net
 

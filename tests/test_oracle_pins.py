@@ -519,6 +519,13 @@ def _torch_dense(net, x):
             y = Fnn.avg_pool2d(xs[0], L.kh, L.stride, L.pad, count_include_pad=True)
         elif L.op == "up":
             y = Fnn.interpolate(xs[0], scale_factor=L.up, mode="nearest")
+        elif L.op == "convtranspose":
+            w = torch.from_numpy(np.asarray(L.weight, np.float64)).permute(3, 0, 1, 2)   # [C_in, C_out, kh, kw]
+            y = Fnn.conv_transpose2d(xs[0], w, torch.from_numpy(np.asarray(L.bias, np.float64)),
+                                     stride=L.stride, padding=L.pad)
+            y = acts[L.act](y)
+        elif L.op == "upbilinear":
+            y = Fnn.interpolate(xs[0], scale_factor=L.up, mode="bilinear", align_corners=False)
         elif L.op == "add":
             y = acts[L.act](sum(xs))
         elif L.op == "concat":
@@ -539,3 +546,143 @@ def test_dense_forward_matches_torch_library(seed):
     x = np.random.default_rng(seed).standard_normal((2, net.in_h, net.in_w, net.in_c))
     for a, b in zip(dense_forward(net, x, wdtype="f64"), _torch_dense(net, x)):
         np.testing.assert_allclose(a, b, rtol=1e-11, atol=1e-11)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: bilinear upsampling ("upsampling layers")
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("f", [2, 3, 4])
+def test_bilinear_upsample_matches_torch(f):
+    """Library pin: torch's bilinear interpolation (align_corners=False) in fp64."""
+    import torch
+    from oracle import upsample_bilinear
+    rng = np.random.default_rng(f)
+    x = rng.standard_normal((2, 5, 7, 3))
+    want = torch.nn.functional.interpolate(torch.from_numpy(x).permute(0, 3, 1, 2), scale_factor=f,
+                                           mode="bilinear", align_corners=False).permute(0, 2, 3, 1).numpy()
+    np.testing.assert_allclose(upsample_bilinear(x, f), want, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("f", [2, 3])
+def test_bilinear_mask_brute_force(f):
+    """Output pixel active iff one of its (up to 4) sources with a non-zero weight is active,
+    recounted pixel by pixel from the scalar definition of the taps."""
+    from oracle import mask_up_bilinear
+    rng = np.random.default_rng(10 + f)
+    m = rng.random((2, 6, 5)) < 0.15
+    got = mask_up_bilinear(m, f)
+    H, W = m.shape[1:]
+
+    def taps(o, n):
+        src = max(0.0, (o + 0.5) / f - 0.5)
+        i0 = int(np.floor(src))
+        lam = src - i0
+        out = [(i0, 1.0 - lam)]
+        if lam > 0:
+            out.append((min(i0 + 1, n - 1), lam))
+        return out
+    for s in range(2):
+        for y in range(H * f):
+            for x in range(W * f):
+                want = any(m[s, yy, xx] for yy, wy in taps(y, H) for xx, wx in taps(x, W) if wy * wx > 0)
+                assert got[s, y, x] == want, (s, y, x)
+
+
+def test_bilinear_delta_is_dense_difference():
+    """Linearity (Eq. 1 for a linear op): interpolating the masked deltas equals the difference of
+    the interpolated frames, and every pixel whose interpolated value changed is in the mask."""
+    from oracle import upsample_bilinear, mask_up_bilinear
+    rng = np.random.default_rng(3)
+    x0 = rng.standard_normal((1, 9, 8, 4))
+    m = rng.random((1, 9, 8)) < 0.1
+    x1 = np.where(m[..., None], x0 + rng.standard_normal(x0.shape), x0)
+    d = upsample_bilinear(np.where(m[..., None], x1 - x0, 0.0), 2)
+    np.testing.assert_allclose(d, upsample_bilinear(x1, 2) - upsample_bilinear(x0, 2), atol=1e-12)
+    changed = np.abs(upsample_bilinear(x1, 2) - upsample_bilinear(x0, 2)).max(-1) > 1e-12
+    assert not (changed & ~mask_up_bilinear(m, 2)).any()
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: transposed convolution (Pose-ResNet head, PAPER.md:369)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("k,s,p", [(4, 2, 1), (3, 2, 1), (2, 2, 0), (3, 1, 1)])
+def test_conv_transpose_matches_torch(k, s, p):
+    """Library pin: torch.nn.functional.conv_transpose2d in fp64."""
+    from oracle import conv_transpose2d
+    rng = np.random.default_rng(k * 10 + s)
+    x = rng.standard_normal((2, 5, 6, 3))
+    w = rng.standard_normal((4, k, k, 3))
+    b = rng.standard_normal(4)
+    want = Fnn.conv_transpose2d(torch.from_numpy(x).permute(0, 3, 1, 2), torch.from_numpy(w).permute(3, 0, 1, 2),
+                                torch.from_numpy(b), stride=s, padding=p).permute(0, 2, 3, 1).numpy()
+    np.testing.assert_allclose(conv_transpose2d(x, w, b, s, p), want, rtol=0, atol=1e-12)
+
+
+def test_conv_transpose_hand_example():
+    """Hand-computed: a single 1 at input (1, 1), stride 2, pad 1, 4x4 kernel w[ky, kx] = 10 ky + kx
+    lands at outputs p = q * 2 - 1 + k, i.e. rows / cols 1..4, with value w[p - 1]."""
+    from oracle import conv_transpose2d
+    x = np.zeros((1, 3, 3, 1))
+    x[0, 1, 1, 0] = 1.0
+    w = np.array([[10.0 * ky + kx for kx in range(4)] for ky in range(4)]).reshape(1, 4, 4, 1)
+    y = conv_transpose2d(x, w, None, 2, 1)[0, :, :, 0]
+    assert y.shape == (6, 6)
+    want = np.zeros((6, 6))
+    for ky in range(4):
+        for kx in range(4):
+            want[1 + ky, 1 + kx] = 10 * ky + kx
+    np.testing.assert_array_equal(y, want)
+
+
+def test_conv_transpose_mask_brute_force():
+    from oracle import mask_conv_transpose
+    rng = np.random.default_rng(7)
+    m = rng.random((2, 5, 4)) < 0.2
+    got = mask_conv_transpose(m, 4, 4, 2, 1)
+    S, H, W = m.shape
+    want = np.zeros_like(got)
+    for s_ in range(S):
+        for qy in range(H):
+            for qx in range(W):
+                if m[s_, qy, qx]:
+                    for ky in range(4):
+                        for kx in range(4):
+                            py, px = qy * 2 - 1 + ky, qx * 2 - 1 + kx
+                            if 0 <= py < got.shape[1] and 0 <= px < got.shape[2]:
+                                want[s_, py, px] = True
+    np.testing.assert_array_equal(got, want)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1: depthwise convolution (PAPER.md:661-667) and EfficientDet-Lite0 (PAPER.md:376)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("k,s", [(3, 1), (5, 2)])
+def test_depthwise_conv_matches_torch(k, s):
+    """Library pin: torch F.conv2d with groups = C (fp64)."""
+    rng = np.random.default_rng(k + s)
+    x = rng.standard_normal((2, 9, 11, 8))
+    w = rng.standard_normal((8, k, k, 1))
+    b = rng.standard_normal(8)
+    want = Fnn.conv2d(torch.from_numpy(x).permute(0, 3, 1, 2), torch.from_numpy(w).permute(0, 3, 1, 2),
+                      torch.from_numpy(b), stride=s, padding=k // 2, groups=8).permute(0, 2, 3, 1).numpy()
+    np.testing.assert_allclose(conv2d(x, w, b, s, k // 2, 1, 8), want, rtol=0, atol=1e-12)
+
+
+def test_efficientdet_lite0_table_and_eps0_equivalence():
+    """EfficientDet-Lite0 layer table (B0 stage table without SE: 16 MBConv blocks, 80 depthwise
+    convs incl. BiFPN / head separable convs, ~3.3 M parameters with a 20-class head) and, on a
+    128 x 128 input, delta output == dense inference at eps = 0 (Eq. 1 + Eqs. 4-6), fp64."""
+    net = nets.efficientdet_lite0(128, 128, eps=0.0, input_eps=0.0, input_dilation=0, dtype="f64")
+    convs = [L for L in net.layers if L.op == "conv"]
+    assert len(convs) == 179 and sum(L.groups > 1 for L in convs) == 80
+    assert max(L.c_out for L in convs) == 1152
+    assert abs(net.n_params() - 3.31e6) < 0.02e6
+    fr = clip([VideoSpec(128, 128, n_blobs=2, blob_h=12, blob_w=9, speed=3, seed=s) for s in (1, 2)], 3)
+    o = DeltaOracle(net, 2, storage="f64")
+    for t in range(fr.shape[0]):
+        outs = o.step(fr[t])
+        for a, b in zip(outs, dense_forward(net, fr[t], wdtype="f64")):
+            np.testing.assert_allclose(a, b, rtol=1e-10, atol=1e-10 * (1 + np.abs(b).max()))

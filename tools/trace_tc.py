@@ -21,7 +21,8 @@ if __name__ == "__main__":
         act = cfg[7] if len(cfg) > 7 else "relu"
         b = nets._Builder("c", H, W, ci, 0, "f16")
         i = b.conv(-1, co, k, stride=s, act=act)
-        b.net.outputs = [i]
+        # a non-output conv (an identity 1x1 max-pool consumes it), like the convs inside a net
+        b.net.outputs = [b.maxpool(i, 1, 1, 0)] if os.environ.get("TRACE_INNER", "1") == "1" else [i]
         b.net.input_eps = -1.0
         eng = DeltaNet(b.net, S)
         x = torch.randn(S, H, W, ci).half().cuda()
