@@ -129,7 +129,7 @@ typedef struct {
   int32_t input_dilation;         /* Chebyshev radius r of the input-mask dilation  */
   int32_t n_layers;
   const dcnn_layer_desc* layers;  /* topological order                                       */
-  int32_t n_outputs;
+  int32_t n_outputs;       /* 1..16 */
   const int32_t* output_ops;      /* ops whose dense accumulated output O is returned */
   int32_t flags;                  /* DCNN_FLAG_*                                              */
 } dcnn_net_desc;

@@ -18,6 +18,10 @@ Readings of the paper adopted here:
   Z9  max-pool caches its accumulated (pre-pool) input; Eq. 3 with f = pool
   Z10 add/concat: mask union, an absent operand contributes 0
   Z11 nearest upsample replicates delta and mask
+  Z11-b bilinear upsample (align_corners = false) interpolates the masked deltas (linear); its
+      mask is the OR of the sources with non-zero weight (NEXT-4)
+  R-convT transposed conv by its scatter definition; mask = scatter-OR of the input mask (NEXT-4)
+  R-dw depthwise conv = conv2d with groups = C (NEXT-1)
   Z12 storage rounding (fp16/fp32) is applied where the method stores a value
   Z22 eps < 0 never truncates; eps_in < 0 marks every input pixel
 """

@@ -729,7 +729,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
     o.Ci_real = o.Ci;
     if (o.in[0] < 0) o.Ci = n->inCp;
   }
-  if (d->n_outputs > MAX_OUT) return fail(DCNN_ERR_UNSUPPORTED, "at most 8 output ops");
+  if (d->n_outputs > MAX_OUT) return fail(DCNN_ERR_UNSUPPORTED, "at most 16 output ops");
   for (int k = 0; k < d->n_outputs; ++k) {
     int j = d->output_ops[k];
     if (j < 0 || j >= L) return fail(DCNN_ERR_ARG, "output op index");
@@ -811,6 +811,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
       CUDA_TRY(cudaMemset(o.O, 0, px * o.ld * sizeof(float)));
     }
     if (o.kind == DCNN_OP_CONV) {
+      o.Cp = (o.C + 3) / 4 * 4;                             // (plan_cc sets it too)
       if (o.C <= 32 * MAXK && (r = plan_cc(o))) return r;   // (wider: tensor cores only)
       o.tS = S; o.tH = o.H; o.tW = o.W; o.tHi = o.Hi; o.tWi = o.Wi;
       {
@@ -863,7 +864,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
       if ((r = dalloc(n, &o.bias, o.ld * 4))) return r;
       CUDA_TRY(cudaMemcpy(o.bias, b.data(), o.ld * 4, cudaMemcpyHostToDevice));
       const size_t smem = cc_smem(o);
-      if (smem > 200 * 1024) return fail(DCNN_ERR_UNSUPPORTED, "conv tile does not fit shared memory");
+      if (o.C <= 32 * MAXK && smem > 200 * 1024) return fail(DCNN_ERR_UNSUPPORTED, "conv tile does not fit shared memory");
       if (o.tc) {
         ConvTCParams& p = o.tcp;
         p.S = o.tS; p.H = o.tHi; p.W = o.tWi; p.Ci = o.Ci; p.Ho = o.tH; p.Wo = o.tW; p.Co = o.C;
@@ -949,6 +950,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
     }
     if (o.kind == DCNN_OP_CONV) {
       o.smax = (n->flags & DCNN_FLAG_PER_PIXEL) ? (1 << 30) : (n->flags & DCNN_FLAG_HYBRID_DISPATCH) ? 4 : 0;
+      if (o.C > 32 * MAXK) o.smax = 0;      // wider than the CUDA-core epilogues: tensor cores only
       if (o.smax) {
         ConvCCParams q;
         memset(&q, 0, sizeof(q));

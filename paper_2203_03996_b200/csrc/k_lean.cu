@@ -498,10 +498,14 @@ __global__ void __launch_bounds__(256) k_copy_out(OutCopyParams p) {
       const float4* s4 = reinterpret_cast<const float4*>(src);
       float4* d4 = reinterpret_cast<float4*>(dst);
       for (long long i = tid; i < n / 4; i += nth) d4[i] = s4[i];
-    } else {                                   // padded head rows (ld > C) or unaligned buffers
-      for (long long i = tid; i < n; i += nth) {
-        const long long r = i / p.C[k];
-        dst[i] = src[r * p.ld[k] + (i - r * p.C[k])];
+    } else {                                   // padded head rows (ld > C) or unaligned buffers:
+      const int lane = threadIdx.x & 31;       // one warp per row, lanes over its channels
+      const long long nw = nth >> 5;           // (no per-element division; coalesced both sides)
+      const int C = p.C[k], ld = p.ld[k];
+      for (long long r = tid >> 5; r < p.rows[k]; r += nw) {
+        const float* s = src + r * ld;
+        float* d = dst + r * C;
+        for (int c = lane; c < C; c += 32) d[c] = s[c];
       }
     }
   }

@@ -175,7 +175,7 @@ void launch_up_lean(const PwParams& p, cudaStream_t st);
 // ---------------------------------------------------------------- outputs
 // Copy of the dense outputs O (fp32, rows at pitch ld) into the caller's buffers (rows of C),
 // the last node of the frame graph (PDL-chained, destinations updated per call)
-constexpr int MAX_OUT = 8;
+constexpr int MAX_OUT = 16;
 struct OutCopyParams {
   int n;
   const float* src[MAX_OUT];
