@@ -174,6 +174,24 @@ DCNN_API dcnn_status dcnn_process_frame(dcnn_net* net, const void* frames, void*
 DCNN_API dcnn_status dcnn_process_frame_host(dcnn_net* net, const void* host_frames,
                                     void* const* host_outputs, void* stream);
 
+/* Pipelined host I/O (end-to-end throughput): enqueue one frame from HOST memory and return
+ * without waiting.  The frame's host->device copy runs on an internal copy stream while the
+ * previous frame computes on `stream`; its outputs are written by the frame graph into one of
+ * two device staging slots and copied device->host on a second copy stream while the next frame
+ * computes.  Frames are processed in submission order with the same semantics as
+ * dcnn_process_frame.
+ *   host_frames  : [S,in_h,in_w,in_c] in desc.dtype; should be pinned (page-locked) for the
+ *                  copies to be asynchronous.  Must stay unchanged until the frame's completion.
+ *   host_outputs : n_outputs pinned buffers, each [S,Ho,Wo,Co] fp32 (compact); valid after
+ *                  dcnn_wait_frames.  Must not be freed before that.
+ *   errors       : argument errors synchronous; device errors sticky, reported by the next
+ *                  call or by dcnn_wait_frames.  Not available while kernel timing is enabled. */
+DCNN_API dcnn_status dcnn_submit_frame_host(dcnn_net* net, const void* host_frames,
+                                            void* const* host_outputs, void* stream);
+
+/* Block until every frame submitted with dcnn_submit_frame_host has its outputs in host memory. */
+DCNN_API dcnn_status dcnn_wait_frames(dcnn_net* net);
+
 /* Flush the caches of one stream (or all with -1): its next frame is dense
  * again (PAPER.md:715-719 S1.4).  No device work is enqueued here: the request is
  * recorded on the host and applied on the stream of the NEXT process_frame call,

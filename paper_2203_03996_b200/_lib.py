@@ -49,7 +49,8 @@ class dcnn_op_stats(C.Structure):
 
 EXPORTS = ["dcnn_create_net", "dcnn_set_threshold", "dcnn_process_frame",
            "dcnn_process_frame_host", "dcnn_reset", "dcnn_destroy_net", "dcnn_op_shape",
-           "dcnn_get_stats", "dcnn_debug_read", "dcnn_kernels_per_frame", "dcnn_last_error"]
+           "dcnn_get_stats", "dcnn_debug_read", "dcnn_kernels_per_frame", "dcnn_last_error",
+           "dcnn_submit_frame_host", "dcnn_wait_frames"]
 
 _lib = None
 
@@ -68,6 +69,8 @@ def load_library(path: str = LIB_PATH):
     lib.dcnn_set_threshold.argtypes = [vp, C.c_int32, C.c_float]
     lib.dcnn_process_frame.argtypes = [vp, vp, C.POINTER(vp), vp]
     lib.dcnn_process_frame_host.argtypes = [vp, vp, C.POINTER(vp), vp]
+    lib.dcnn_submit_frame_host.argtypes = [vp, vp, C.POINTER(vp), vp]
+    lib.dcnn_wait_frames.argtypes = [vp]
     lib.dcnn_reset.argtypes = [vp, C.c_int32]
     lib.dcnn_destroy_net.argtypes = [vp]
     lib.dcnn_destroy_net.restype = None
@@ -87,7 +90,8 @@ def load_library(path: str = LIB_PATH):
     for name in ["dcnn_create_net", "dcnn_set_threshold", "dcnn_process_frame",
                  "dcnn_process_frame_host", "dcnn_reset", "dcnn_op_shape", "dcnn_get_stats",
                  "dcnn_debug_read", "dcnn_enable_kernel_timing", "dcnn_kernel_timing",
-                 "dcnn_debug_poison", "dcnn_debug_tc_trace", "dcnn_debug_launch_times"]:
+                 "dcnn_debug_poison", "dcnn_debug_tc_trace", "dcnn_debug_launch_times",
+                 "dcnn_submit_frame_host", "dcnn_wait_frames"]:
         getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -202,6 +206,24 @@ class DeltaNet:
         _check(self.lib, self.lib.dcnn_process_frame_host(self.h, C.c_void_p(fr.ctypes.data), optr,
                                                           C.c_void_p(sp)))
         return outputs
+
+    def submit_frame_host(self, frames: np.ndarray, outputs, stream=None):
+        """Pipelined host I/O (dcnn_submit_frame_host): enqueue frames (pinned numpy, net dtype,
+        [S,H,W,C]) and return; ``outputs`` (pinned fp32 numpy, one per output op) are filled
+        once ``wait_frames()`` returns.  Both must stay alive until then."""
+        fshape = (self.S, self.net.in_h, self.net.in_w, self.net.in_c)
+        want = np.float16 if self.dtype == "f16" else np.float32
+        if frames.dtype != want or frames.shape != fshape or not frames.flags.c_contiguous:
+            raise ValueError(f"frames must be a contiguous {np.dtype(want)} array of shape {fshape}")
+        self._check_outputs(outputs, lambda o: (isinstance(o, np.ndarray) and o.dtype == np.float32
+                                                and o.flags.c_contiguous, o.shape))
+        optr = (C.c_void_p * len(outputs))(*[o.ctypes.data for o in outputs])
+        sp = 0 if stream is None else stream.cuda_stream
+        _check(self.lib, self.lib.dcnn_submit_frame_host(self.h, C.c_void_p(frames.ctypes.data), optr,
+                                                         C.c_void_p(sp)))
+
+    def wait_frames(self):
+        _check(self.lib, self.lib.dcnn_wait_frames(self.h))
 
     def _check_outputs(self, outputs, props):
         """One fp32 contiguous buffer of S*Ho*Wo*Co elements per output op (the library writes

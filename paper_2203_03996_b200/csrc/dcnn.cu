@@ -133,6 +133,14 @@ struct dcnn_net {
   // host staging for the _host entry point
   void* h_frames = nullptr;
   size_t frame_bytes = 0;
+  // pipelined host I/O (dcnn_submit_frame_host): two slots of a device frame buffer and compact
+  // device output staging, an H2D and a D2H stream, and per-slot events
+  bool pipe_init = false;
+  long long pipe_t = 0;
+  void* pipe_frame[2] = {nullptr, nullptr};
+  std::vector<float*> pipe_out[2];
+  cudaStream_t pipe_h2d = nullptr, pipe_d2h = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_graph[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
   // branch streams used during graph capture
   std::vector<cudaStream_t> aux;
   std::vector<cudaEvent_t> ev_done, ev_join;
@@ -199,6 +207,7 @@ static bool plan_tc(Op& o, int dtype, int flags) {
   static const int max_split = getenv("DCNN_TC_MAX_SPLIT") ? atoi(getenv("DCNN_TC_MAX_SPLIT")) : 8;
   static const bool no_resident = getenv("DCNN_TC_NO_RESIDENT") != nullptr;
   static const int force_nab = getenv("DCNN_TC_NAB") ? atoi(getenv("DCNN_TC_NAB")) : 0;   // A/B: halo buffers
+  static const bool s2_nab2 = getenv("DCNN_TC_S2_NAB2") != nullptr;   // A/B: allow 2 halo buffers at stride 2
   p.dbg = getenv("DCNN_TC_DBG") ? atoi(getenv("DCNN_TC_DBG")) : 0;
   const int s = o.stride, d = o.dil;
   if (s > 2 || o.kh * o.kw > 64) return false;         // stride phases / tap table
@@ -243,6 +252,10 @@ static bool plan_tc(Op& o, int dtype, int flags) {
           for (int nab = 2; nab <= 4; ++nab) {
             if (nab > 2 && nab > ncb) break;
             if (force_nab && nab != std::min(force_nab, std::max(2, ncb))) continue;
+            // stride 2: a halo block is 16-byte-TMA-request bound (~1.3 ns each; 1188 for 16
+            // channels of a 3x3 s2 tile), so keep >= 2 blocks in flight (YOLOv5s 40x40x256 s2:
+            // K loop 79 -> 51 us, profiles/r02_trace_s2_convs_nab.txt)
+            if (s == 2 && nab == 2 && ncb >= 3 && !s2_nab2) continue;
             double wb;
             int stages;
             if (resident) {
@@ -597,6 +610,13 @@ void dcnn_destroy_net(dcnn_net* n) {
     cudaEventDestroy(t.b);
   }
   if (n->h_frames) cudaFreeHost(n->h_frames);
+  if (n->pipe_h2d) cudaStreamDestroy(n->pipe_h2d);
+  if (n->pipe_d2h) cudaStreamDestroy(n->pipe_d2h);
+  for (int k = 0; k < 2; ++k) {
+    if (n->ev_h2d[k]) cudaEventDestroy(n->ev_h2d[k]);
+    if (n->ev_graph[k]) cudaEventDestroy(n->ev_graph[k]);
+    if (n->ev_d2h[k]) cudaEventDestroy(n->ev_d2h[k]);
+  }
   delete n;
 }
 
@@ -1228,6 +1248,70 @@ dcnn_status dcnn_process_frame_host(dcnn_net* n, const void* host_frames, void* 
   }
   n->last = st;
   CUDA_TRY(cudaStreamSynchronize(st));
+  return check_err(n);
+}
+
+// Pipelined host I/O: frame t's H2D (slot t mod 2, H2D stream) overlaps frame t-1's compute,
+// and its D2H (D2H stream) overlaps frame t+1's compute.  Slot reuse is ordered by events: the
+// H2D into slot k waits for the graph that last read it, the graph writing slot k's output
+// staging waits for the D2H that last read it.
+dcnn_status dcnn_submit_frame_host(dcnn_net* n, const void* host_frames, void* const* host_outputs, void* stream) {
+  if (!n || !host_frames || !host_outputs) return fail(DCNN_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(n->device));
+  if (n->timing_mask) return fail(DCNN_ERR_ARG, "submit_frame_host is not available with kernel timing");
+  dcnn_status s = check_err(n);
+  if (s) return s;
+  if ((s = build_graph(n))) return s;
+  if (!n->pipe_init) {
+    for (int k = 0; k < 2; ++k) {
+      if ((s = dalloc(n, &n->pipe_frame[k], n->frame_bytes))) return s;
+      for (int o : n->outputs) {
+        float* b = nullptr;
+        const Op& op = n->ops[o];
+        if ((s = dalloc(n, &b, (size_t)n->S * op.H * op.W * op.C * 4))) return s;
+        n->pipe_out[k].push_back(b);
+      }
+      CUDA_TRY(cudaEventCreateWithFlags(&n->ev_h2d[k], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&n->ev_graph[k], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&n->ev_d2h[k], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaStreamCreateWithFlags(&n->pipe_h2d, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&n->pipe_d2h, cudaStreamNonBlocking));
+    n->pipe_init = true;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int k = (int)(n->pipe_t & 1);
+  if (n->pipe_t >= 2) CUDA_TRY(cudaStreamWaitEvent(n->pipe_h2d, n->ev_graph[k], 0));   // slot k read
+  CUDA_TRY(cudaMemcpyAsync(n->pipe_frame[k], host_frames, n->frame_bytes, cudaMemcpyHostToDevice, n->pipe_h2d));
+  CUDA_TRY(cudaEventRecord(n->ev_h2d[k], n->pipe_h2d));
+  if ((s = apply_resets(n, st))) return s;
+  CUDA_TRY(cudaStreamWaitEvent(st, n->ev_h2d[k], 0));
+  if (n->pipe_t >= 2) CUDA_TRY(cudaStreamWaitEvent(st, n->ev_d2h[k], 0));      // staging k drained
+  std::vector<void*> outs(n->pipe_out[k].begin(), n->pipe_out[k].end());
+  if ((s = set_frame_io(n, n->pipe_frame[k], outs.data()))) return s;
+  CUDA_TRY(cudaGraphLaunch(n->exec, st));
+  CUDA_TRY(cudaEventRecord(n->ev_graph[k], st));
+  CUDA_TRY(cudaStreamWaitEvent(n->pipe_d2h, n->ev_graph[k], 0));
+  for (size_t q = 0; q < n->outputs.size(); ++q) {
+    const Op& op = n->ops[n->outputs[q]];
+    if (host_outputs[q])
+      CUDA_TRY(cudaMemcpyAsync(host_outputs[q], n->pipe_out[k][q], (size_t)n->S * op.H * op.W * op.C * 4,
+                               cudaMemcpyDeviceToHost, n->pipe_d2h));
+  }
+  CUDA_TRY(cudaEventRecord(n->ev_d2h[k], n->pipe_d2h));
+  n->last = st;
+  ++n->pipe_t;
+  return DCNN_OK;
+}
+
+dcnn_status dcnn_wait_frames(dcnn_net* n) {
+  if (!n) return fail(DCNN_ERR_ARG, "null net");
+  CUDA_TRY(cudaSetDevice(n->device));
+  if (n->pipe_init) {
+    CUDA_TRY(cudaStreamSynchronize(n->pipe_h2d));
+    CUDA_TRY(cudaStreamSynchronize(n->pipe_d2h));
+  }
+  if (n->last) CUDA_TRY(cudaStreamSynchronize(n->last));
   return check_err(n);
 }
 

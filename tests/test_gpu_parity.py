@@ -222,3 +222,32 @@ def test_input_stage_masks_and_deltas(C, r, dt, eps):
         np.testing.assert_array_equal(np.where(om[..., None], gd, 0.0), np.where(om[..., None], od, 0.0),
                                       err_msg=f"frame {t}: input delta")
     eng.close()
+
+
+def test_pipelined_host_io_matches_device_path():
+    """dcnn_submit_frame_host / dcnn_wait_frames (overlapped H2D / compute / D2H) give the same
+    outputs, bit for bit, as dcnn_process_frame on device buffers, including a reset mid-clip."""
+    net = nets.toy_net(64, 64, 16, eps=0.02)
+    specs = [VideoSpec(64, 64, n_blobs=2, blob_h=8, blob_w=8, seed=s) for s in (11, 12)]
+    frames = clip(specs, 7)
+    a = _engine(net, 2)
+    b = _engine(net, 2)
+    want = []
+    out = [torch.empty((2,) + s, device="cuda") for s in a.out_shapes]
+    for t in range(7):
+        if t == 4:
+            a.reset(0)
+        a.process_frame(torch.from_numpy(frames[t]).cuda(), out)
+        want.append([o.cpu().numpy().copy() for o in out])
+    hf = [torch.from_numpy(np.ascontiguousarray(frames[t])).pin_memory().numpy() for t in range(7)]
+    ho = [[torch.empty((2,) + s, dtype=torch.float32).pin_memory().numpy() for s in b.out_shapes] for _ in range(7)]
+    for t in range(7):
+        if t == 4:
+            b.reset(0)
+        b.submit_frame_host(hf[t], ho[t])
+    b.wait_frames()
+    for t in range(7):
+        for g, w in zip(ho[t], want[t]):
+            np.testing.assert_array_equal(g, w, err_msg=f"frame {t}")
+    a.close()
+    b.close()
