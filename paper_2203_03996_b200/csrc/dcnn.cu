@@ -252,10 +252,11 @@ static bool plan_tc(Op& o, int dtype, int flags) {
           for (int nab = 2; nab <= 4; ++nab) {
             if (nab > 2 && nab > ncb) break;
             if (force_nab && nab != std::min(force_nab, std::max(2, ncb))) continue;
-            // stride 2: a halo block is 16-byte-TMA-request bound (~1.3 ns each; 1188 for 16
-            // channels of a 3x3 s2 tile), so keep >= 2 blocks in flight (YOLOv5s 40x40x256 s2:
-            // K loop 79 -> 51 us, profiles/r02_trace_s2_convs_nab.txt)
-            if (s == 2 && nab == 2 && ncb >= 3 && !s2_nab2) continue;
+            // stride 2 with several streams: a halo block is 16-byte-TMA-request bound (~1.3 ns
+            // each; 1188 for 16 channels of a 3x3 s2 tile), so keep >= 2 blocks in flight
+            // (YOLOv5s 40x40x256 s2: K loop 79 -> 51 us, profiles/r02_trace_s2_convs_nab.txt;
+            // YOLOv5s S = 8 +2.3 %; at S = 1 the other plans win by 2 %, profiles/r02_ab.md)
+            if (s == 2 && nab == 2 && ncb >= 3 && o.tS >= 4 && !s2_nab2) continue;
             double wb;
             int stages;
             if (resident) {
