@@ -104,6 +104,14 @@ typedef struct {
   const float* bias;       /* CONV: host fp32 [c_out] or NULL                            */
   const float* scale;      /* AFFINE: host fp32 [C]                                      */
   const float* shift;      /* AFFINE: host fp32 [C]                                      */
+  /* CONV / CONV_TRANSPOSE: optional batch norm after the conv (all four NULL = none), folded
+   * into the weights and bias at create:
+   *   w'[o] = w[o] * g[o],  b'[o] = (b[o] - mean[o]) * g[o] + beta[o],  g = gamma / sqrt(var + bn_eps) */
+  const float* bn_gamma;   /* host fp32 [c_out] */
+  const float* bn_beta;
+  const float* bn_mean;
+  const float* bn_var;
+  float bn_eps;            /* > 0 (0 -> 1e-5) */
 } dcnn_layer_desc;
 
 enum {

@@ -20,5 +20,5 @@ brute force on tiny inputs.
 from .delta_oracle import (  # noqa: F401
     act_fn, conv2d, mask_conv, maxpool2d, avgpool2d, upsample_nearest, dilate_chebyshev,
     upsample_bilinear, mask_up_bilinear, conv_transpose2d, mask_conv_transpose,
-    dense_forward, DeltaOracle, quantize, tile_window_counts,
+    dense_forward, DeltaOracle, quantize, tile_window_counts, fold_bn,
 )

@@ -22,6 +22,7 @@ Readings of the paper adopted here:
       mask is the OR of the sources with non-zero weight (NEXT-4)
   R-convT transposed conv by its scatter definition; mask = scatter-OR of the input mask (NEXT-4)
   R-dw depthwise conv = conv2d with groups = C (NEXT-1)
+  R-bn batch norm after a conv is folded into its weights and bias (fold_bn)
   Z12 storage rounding (fp16/fp32) is applied where the method stores a value
   Z22 eps < 0 never truncates; eps_in < 0 marks every input pixel
 """
@@ -216,9 +217,26 @@ def dilate_chebyshev(m, r):
 # ---------------------------------------------------------------------------
 
 
+def fold_bn(w, b, bn):
+    """Batch norm folded into the preceding conv ("convolutional layers and batch
+    normalization layers were fused"): with g = gamma / sqrt(var + eps),
+    w'[o] = w[o] * g[o] and b'[o] = (b[o] - mean[o]) * g[o] + beta[o].  fp64."""
+    gamma, beta, mean, var, eps = (np.asarray(v, np.float64) for v in bn)
+    g = gamma / np.sqrt(var + eps)
+    w = np.asarray(w, np.float64) * g.reshape((-1,) + (1,) * (np.ndim(w) - 1))
+    b = (np.zeros_like(g) if b is None else np.asarray(b, np.float64)) - mean
+    return w, b * g + beta
+
+
 def _weights(L, dtype):
-    w = quantize(L.weight, dtype if dtype != "f64" else "f64")
+    w = np.asarray(L.weight, dtype=np.float32).astype(np.float64)
     b = None if L.bias is None else np.asarray(L.bias, dtype=np.float32).astype(np.float64)
+    if getattr(L, "bn", None) is not None:                   # folded, then stored in dtype
+        w, b = fold_bn(w, b, tuple(np.asarray(v, np.float32) if i < 4 else v for i, v in enumerate(L.bn)))
+        if dtype != "f64":                                     # folded values are fp32 inputs of
+            b = b.astype(np.float32).astype(np.float64)        # the method (then rounded to dtype)
+            w = w.astype(np.float32).astype(np.float64)
+    w = quantize(w, dtype if dtype != "f64" else "f64")
     return w, b
 
 

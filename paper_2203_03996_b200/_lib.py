@@ -30,7 +30,10 @@ class dcnn_layer_desc(C.Structure):
                 ("groups", C.c_int32), ("up_factor", C.c_int32), ("act", C.c_int32),
                 ("act_param", C.c_float), ("threshold", C.c_float),
                 ("weight", C.POINTER(C.c_float)), ("bias", C.POINTER(C.c_float)),
-                ("scale", C.POINTER(C.c_float)), ("shift", C.POINTER(C.c_float))]
+                ("scale", C.POINTER(C.c_float)), ("shift", C.POINTER(C.c_float)),
+                ("bn_gamma", C.POINTER(C.c_float)), ("bn_beta", C.POINTER(C.c_float)),
+                ("bn_mean", C.POINTER(C.c_float)), ("bn_var", C.POINTER(C.c_float)),
+                ("bn_eps", C.c_float)]
 
 
 class dcnn_net_desc(C.Structure):
@@ -158,6 +161,13 @@ class DeltaNet:
                     a = np.ascontiguousarray(v, dtype=np.float32)
                     self._keep.append(a)
                     setattr(d, name, _fptr(a))
+            bn = getattr(Ly, "bn", None)
+            if bn is not None:                     # (gamma, beta, mean, var, eps): folded at create
+                for name, v in zip(("bn_gamma", "bn_beta", "bn_mean", "bn_var"), bn[:4]):
+                    a = np.ascontiguousarray(v, dtype=np.float32)
+                    self._keep.append(a)
+                    setattr(d, name, _fptr(a))
+                d.bn_eps = float(bn[4])
         outs = (C.c_int32 * len(net.outputs))(*net.outputs)
         desc = dcnn_net_desc(net.in_h, net.in_w, net.in_c, n_streams, device, DTYPES[net.dtype],
                              net.input_eps, net.input_dilation, L, arr, len(net.outputs), outs, flags)

@@ -1067,9 +1067,51 @@ dcnn_status dcnn_create_net(const dcnn_net_desc* desc, dcnn_net** out) {
   std::vector<std::vector<float>> wflip;
   std::vector<int> umap(Lu), uinv;
   wflip.reserve(Lu);
+  std::vector<std::vector<float>> bnfold;     // folded weights / biases (batch norm at create)
+  bnfold.reserve(2 * Lu);
   for (int i = 0; i < Lu; ++i) {
     dcnn_layer_desc d = desc->layers[i];
     const int nin = (d.op == DCNN_OP_ADD || d.op == DCNN_OP_CONCAT) ? d.n_in : 1;
+    const bool has_bn = d.bn_gamma || d.bn_beta || d.bn_mean || d.bn_var;
+    if (has_bn) {
+      if (!(d.bn_gamma && d.bn_beta && d.bn_mean && d.bn_var) || !d.weight ||
+          (d.op != DCNN_OP_CONV && d.op != DCNN_OP_CONV_TRANSPOSE) || d.c_out <= 0 || d.bn_eps < 0.f)
+        return fail(DCNN_ERR_ARG, "layer " + std::to_string(i) + ": batch norm needs gamma, beta, mean, var on a conv");
+      // fold in double precision: w' = w g, b' = (b - mean) g + beta
+      const double beps = d.bn_eps > 0.f ? d.bn_eps : 1e-5;
+      int cin = 0;                              // weight elements per output channel / (kh kw)
+      {
+        int C;
+        // input channels of this layer (through the caller's indexing; expanded descs keep shapes)
+        std::vector<int> ch(i);
+        for (int k = 0; k < i; ++k) {
+          const dcnn_layer_desc& e = desc->layers[k];
+          const int c0 = e.in[0] < 0 ? desc->in_c : ch[e.in[0]];
+          if (e.op == DCNN_OP_CONV || e.op == DCNN_OP_CONV_TRANSPOSE) ch[k] = e.c_out;
+          else if (e.op == DCNN_OP_CONCAT) {
+            int t = 0;
+            for (int j = 0; j < e.n_in; ++j) t += e.in[j] < 0 ? desc->in_c : ch[e.in[j]];
+            ch[k] = t;
+          } else ch[k] = c0;
+        }
+        C = d.in[0] < 0 ? desc->in_c : (d.in[0] < i ? ch[d.in[0]] : 0);
+        const int g = (d.op == DCNN_OP_CONV && d.groups > 0) ? d.groups : 1;
+        cin = C / g;
+      }
+      const size_t per_o = (size_t)d.kh * d.kw * cin;
+      bnfold.emplace_back((size_t)d.c_out * per_o);
+      std::vector<float>& w = bnfold.back();
+      bnfold.emplace_back((size_t)d.c_out);
+      std::vector<float>& b = bnfold.back();
+      for (int o = 0; o < d.c_out; ++o) {
+        const double g = (double)d.bn_gamma[o] / std::sqrt((double)d.bn_var[o] + beps);
+        for (size_t e = 0; e < per_o; ++e) w[o * per_o + e] = (float)((double)d.weight[o * per_o + e] * g);
+        b[o] = (float)(((d.bias ? (double)d.bias[o] : 0.0) - (double)d.bn_mean[o]) * g + (double)d.bn_beta[o]);
+      }
+      d.weight = w.data();
+      d.bias = b.data();
+      d.bn_gamma = d.bn_beta = d.bn_mean = d.bn_var = nullptr;
+    }
     for (int j = 0; j < nin && j < 4; ++j)
       if (d.in[j] >= 0 && d.in[j] < i) d.in[j] = umap[d.in[j]];
       else if (d.in[j] >= i) return fail(DCNN_ERR_SHAPE, "layer " + std::to_string(i) + ": dangling input reference");

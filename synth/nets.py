@@ -42,6 +42,7 @@ class Layer:
     bias: Optional[np.ndarray] = None
     scale: Optional[np.ndarray] = None   # affine
     shift: Optional[np.ndarray] = None   # affine
+    bn: Optional[tuple] = None           # conv: (gamma, beta, mean, var, eps), folded by the engine
     name: str = ""
 
     @property
@@ -613,6 +614,20 @@ def efficientdet_lite0(H: int = 384, W: int = 384, eps: float = 0.05, input_eps:
     b.net.input_dilation = input_dilation
     b.net.set_inner_eps(eps)
     return b.net
+
+
+def with_batchnorm(net: Net, seed: int = 0) -> Net:
+    """Attach a random inference-mode batch norm to every conv (gamma ~ U(0.5, 1.5), beta ~
+    U(-0.2, 0.2), running mean ~ N(0, 0.2), var ~ U(0.5, 2)): the engine folds it at create
+    (SPEC S:250); the oracle folds it with the same definition (oracle.fold_bn)."""
+    rng = np.random.default_rng(seed + 500)
+    for L in net.layers:
+        if L.op in ("conv", "convtranspose"):
+            c = L.c_out
+            L.bn = (rng.uniform(0.5, 1.5, c).astype(np.float32), rng.uniform(-0.2, 0.2, c).astype(np.float32),
+                    (rng.standard_normal(c) * 0.2).astype(np.float32), rng.uniform(0.5, 2.0, c).astype(np.float32),
+                    1e-3)
+    return net
 
 
 def make_net(name: str, **kw) -> Net:

@@ -251,3 +251,17 @@ def test_pipelined_host_io_matches_device_path():
             np.testing.assert_array_equal(g, w, err_msg=f"frame {t}")
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("dtype,tol,masks", [("f32", 1e-4, "exact"), ("f16", 2e-2, "replay")])
+def test_batchnorm_folded_at_create(dtype, tol, masks):
+    """Every conv (incl. a transposed one) carries an inference-mode batch norm that
+    dcnn_create_net folds into its weights; parity against the
+    oracle's fold definition (oracle.fold_bn), fp32 at eps = 0 with exact masks."""
+    from helpers import lockstep
+    eps = 0.0 if dtype == "f32" else 0.05
+    net = nets.with_batchnorm(nets.pose_resnet_head(64, 48, 16, eps=eps, dtype=dtype), seed=5)
+    dt = np.float16 if dtype == "f16" else np.float32
+    fr = clip([VideoSpec(64, 48, n_blobs=2, blob_h=10, blob_w=8, speed=3, seed=s) for s in (13, 14)], 5, dt)
+    rec, _ = lockstep(net, fr, tol=tol, masks=masks, name=f"batchnorm_fold_{dtype}")
+    print(rec)

@@ -105,7 +105,8 @@ def test_deep_nets_fp16_tensor_cores_eps005(make):
 
 @pytest.mark.parametrize("eps", [0.0, 0.05])
 @pytest.mark.parametrize("k,s,ci,co,act", [(3, 1, 32, 64, "silu"), (1, 1, 64, 64, "silu"),
-                                           (3, 2, 32, 32, "relu")])
+                                           (3, 2, 32, 32, "relu"), (3, 2, 64, 64, "silu"),
+                                           (3, 2, 128, 256, "silu")])
 def test_tc_single_conv_multi_tile(eps, k, s, ci, co, act):
     """>= 200 output tiles (160 x 160 at 16 x 8 per tile): every CTA runs >= 2 tiles."""
     H = W = 160 * s

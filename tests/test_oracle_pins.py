@@ -686,3 +686,26 @@ def test_efficientdet_lite0_table_and_eps0_equivalence():
         outs = o.step(fr[t])
         for a, b in zip(outs, dense_forward(net, fr[t], wdtype="f64")):
             np.testing.assert_allclose(a, b, rtol=1e-10, atol=1e-10 * (1 + np.abs(b).max()))
+
+
+def test_bn_fold_matches_unfused_torch_batchnorm():
+    """T11: a conv with a folded batch norm == torch conv2d followed
+    by F.batch_norm in inference mode (fp64 library routines), <= 1e-12; and the delta path of a
+    net whose every conv carries a batch norm equals its dense inference at eps = 0."""
+    net = nets.with_batchnorm(nets.toy_net(32, 32, 8, eps=0.0, dtype="f64"), seed=3)
+    x = np.random.default_rng(1).standard_normal((2, 32, 32, 3))
+    L = net.layers[0]
+    gamma, beta, mean, var, eps = L.bn
+    xt = torch.from_numpy(x).permute(0, 3, 1, 2)
+    z = Fnn.conv2d(xt, torch.from_numpy(L.weight.astype(np.float64)).permute(0, 3, 1, 2),
+                   torch.from_numpy(L.bias.astype(np.float64)), padding=L.pad)
+    want = Fnn.relu(Fnn.batch_norm(z, torch.from_numpy(mean.astype(np.float64)), torch.from_numpy(var.astype(np.float64)),
+                                   torch.from_numpy(gamma.astype(np.float64)), torch.from_numpy(beta.astype(np.float64)),
+                                   training=False, eps=eps)).permute(0, 2, 3, 1).numpy()
+    one = nets.Net("c", 32, 32, 3, [net.layers[0]], [0], dtype="f64")
+    np.testing.assert_allclose(dense_forward(one, x, wdtype="f64")[0], want, rtol=0, atol=1e-12)
+    fr = clip([VideoSpec(32, 32, n_blobs=2, blob_h=7, blob_w=5, seed=4)], 5)
+    o = DeltaOracle(net, 1, storage="f64")
+    for t in range(fr.shape[0]):
+        for a, b in zip(o.step(fr[t]), dense_forward(net, fr[t], wdtype="f64")):
+            np.testing.assert_allclose(a, b, rtol=1e-10, atol=1e-10 * (1 + np.abs(b).max()))
