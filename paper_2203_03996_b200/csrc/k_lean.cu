@@ -252,6 +252,87 @@ __global__ void __launch_bounds__(256) k_maxpool_win(PwParams p, int lg_nch) {
   warp_count_flush(p.ep.n_active, lane, n);
 }
 
+// Overlapping max-pool (Eq. 3) with the window staged in shared memory: a block owns an 8 x 8
+// output tile x 4 channel chunks (32 channels) of one stream; the (8 + K - 1)^2 input pixels'
+// accumulated inputs A, deltas and update flags are loaded once (every load in flight together)
+// instead of K^2 times per output, then each thread reduces its K x K window from shared memory.
+// Same maxima in the same order as k_maxpool_win (bit-identical).  Stride 1, pad K / 2, C % 32 == 0.
+template <typename T, typename TC, int KK>
+__global__ void __launch_bounds__(256) k_maxpool_tile(PwParams p) {
+  constexpr int TW = 8, HW = TW + KK - 1, NPX = HW * HW;
+  __shared__ uint4 sd[NPX][4], sa[NPX][4];   // [halo pixel][chunk] deltas / accumulated inputs (fp16 x 8)
+  __shared__ uint8_t sm[NPX];
+  pdl_trigger();
+  pdl_wait();
+  frame_bookkeeping(p.ep);
+  const int C = p.ep.C;
+  const int ntx = (p.W + TW - 1) / TW, nty = (p.H + TW - 1) / TW, ncg = C / 32;
+  int b = blockIdx.x;
+  const int cg = b % ncg; b /= ncg;
+  const int tx = b % ntx; b /= ntx;
+  const int ty = b % nty;
+  const int s = b / nty;
+  const int pad = KK / 2;
+  const int iy0 = ty * TW - pad, ix0 = tx * TW - pad;
+  const bool first = p.ep.first[s] != 0;
+  const long long sbase = (long long)s * p.Hi * p.Wi;
+  const T* din = reinterpret_cast<const T*>(p.in[0]);
+  const TC* A = reinterpret_cast<const TC*>(p.poolA);
+  static_assert(sizeof(TC) == 2, "fp16 caches");
+  // stage: halo pixel x chunk items, all loads issued before any store
+  for (int it = threadIdx.x; it < NPX * 4; it += 256) {
+    const int px = it >> 2, c = it & 3;
+    const int iy = iy0 + px / HW, ix = ix0 + px % HW;
+    uint4 dv = make_uint4(0u, 0u, 0u, 0u), av = make_uint4(0u, 0u, 0u, 0u);
+    uint8_t mk = 0;                            // bit 1: inside the image, bit 0: updated
+    if (iy >= 0 && iy < p.Hi && ix >= 0 && ix < p.Wi) {
+      const long long ip = sbase + (long long)iy * p.Wi + ix;
+      const long long off = ip * C + cg * 32 + c * 8;
+      mk = (uint8_t)(2 | ((first || p.min[0][ip]) ? 1 : 0));
+      dv = *reinterpret_cast<const uint4*>(din + off);
+      if (!first) av = *reinterpret_cast<const uint4*>(A + off);   // first frame: A = 0
+    }
+    sd[px][c] = dv;
+    sa[px][c] = av;
+    if (c == 0) sm[px] = mk;
+  }
+  __syncthreads();
+  const int t = threadIdx.x, c = t & 3, o = t >> 2, oy = ty * TW + (o >> 3), ox = tx * TW + (o & 7);
+  const bool valid = oy < p.H && ox < p.W;
+  float mnew[8], mold[8];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) mnew[k] = mold[k] = -INFINITY;
+#pragma unroll
+  for (int ky = 0; ky < KK; ++ky)
+#pragma unroll
+    for (int kx = 0; kx < KK; ++kx) {
+      const int px = ((o >> 3) + ky) * HW + (o & 7) + kx;
+      const uint8_t mk = valid ? sm[px] : 0;
+      if (!(mk & 2)) continue;                 // padding: -inf, never active
+      const bool on = (mk & 1) != 0;
+      any |= on;
+      float d[8], a[8];
+      ld8(reinterpret_cast<const __half*>(&sd[px][c]), d);
+      ld8(reinterpret_cast<const __half*>(&sa[px][c]), a);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        mnew[k] = fmaxf(mnew[k], a[k] + (on ? d[k] : 0.f));
+        mold[k] = fmaxf(mold[k], a[k]);
+      }
+    }
+  const long long q = ((long long)s * p.H + oy) * p.W + ox;
+  if (valid && c == 0 && cg == 0) p.ep.mask[q] = any ? 1 : 0;
+  if (any) {
+    float r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = rnd<T>(first ? mnew[k] : mnew[k] - mold[k]);   // Eq. 3
+    st8(reinterpret_cast<T*>(p.ep.delta) + q * C + cg * 32 + c * 8, r);
+  }
+  const unsigned n = (unsigned)warp_sum((any && c == 0 && cg == 0) ? 1 : 0);
+  warp_count_flush(p.ep.n_active, threadIdx.x & 31, n);
+}
+
 // A := A + dx~ on the active input pixels, 16 bytes per thread (after the pool read old A)
 template <typename T, typename TC>
 __global__ void __launch_bounds__(256) k_pool_update_vec(PwParams p, int lg_nch) {
@@ -505,7 +586,19 @@ __global__ void __launch_bounds__(256) k_copy_out(OutCopyParams p) {
       for (long long r = tid >> 5; r < p.rows[k]; r += nw) {
         const float* s = src + r * ld;
         float* d = dst + r * C;
-        for (int c = lane; c < C; c += 32) d[c] = s[c];
+        for (int c0 = 0; c0 < C; c0 += 256) {   // 8 loads in flight per lane, then the stores
+          float v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = c0 + lane + 32 * j;
+            v[j] = c < C ? s[c] : 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = c0 + lane + 32 * j;
+            if (c < C) d[c] = v[j];
+          }
+        }
       }
     }
   }
@@ -529,7 +622,13 @@ void launch_maxpool_win(const PwParams& p, int cache32, cudaStream_t st) {
   const int lg = log2_exact(p.ep.C / 8);
   const int grid = lean_grid(((long long)p.S * p.H * p.W) << lg);
   const int gridu = lean_grid(((long long)p.S * p.Hi * p.Wi) << lg);
-  if (p.k == 5) {
+  static const bool no_tile = getenv("DCNN_NO_POOL_TILE") != nullptr;
+  if (!no_tile && !cache32 && p.stride == 1 && p.pad == p.k / 2 && p.ep.C % 32 == 0 && p.ep.O == nullptr &&
+      p.H == p.Hi && p.W == p.Wi) {
+    const int blocks = p.S * ((p.H + 7) / 8) * ((p.W + 7) / 8) * (p.ep.C / 32);
+    if (p.k == 5) launch_k(k_maxpool_tile<__half, __half, 5>, dim3(blocks), dim3(256), 0, st, 1, p);
+    else launch_k(k_maxpool_tile<__half, __half, 3>, dim3(blocks), dim3(256), 0, st, 1, p);
+  } else if (p.k == 5) {
     if (cache32) launch_k(k_maxpool_win<__half, float, 5>, dim3(grid), dim3(256), 0, st, 1, p, lg);
     else launch_k(k_maxpool_win<__half, __half, 5>, dim3(grid), dim3(256), 0, st, 1, p, lg);
   } else {
