@@ -302,6 +302,16 @@ def gather_checksums(hs, dist, world):
 
 
 # ------------------------------------------------------------------------- reference arm
+def line_config(args, wl, net, S, world):
+    """The `config` object of the JSON line (the same for the engine and the reference arm)."""
+    return {"workload": f"{args.workload} S={S}/GPU ({wl['cfg']})", "baseline_cfg": wl["cfg"],
+            "model": wl["model"], "streams_per_gpu": S, "frame": [net.in_h, net.in_w, 3],
+            "input_eps": net.input_eps, "input_dilation": net.input_dilation,
+            "inner_eps": max([L.eps for L in net.layers if L.truncates] + [0]),
+            "l2": "flushed (256 MiB write) between timed steps",
+            "parallelism": f"independent camera streams x{world} GPUs (no data-path collective)"}
+
+
 def run_reference(args, wl, rank, world):
     """The CPU oracle as it stands on the host cores; a step = one frame of stream 0 of this
     workload (a bounded sample: the full 8-stream step would take minutes per frame)."""
@@ -326,12 +336,12 @@ def run_reference(args, wl, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": args.workload, "baseline_cfg": wl["cfg"], "streams_per_step": 1,
-                       "model": wl["model"]},
+            "config": line_config(args, wl, net, args.streams or wl["S"], world),
             "cpu_baseline": {"value": v, "unit": "frames/s", "cores": cores, "kind": "oracle",
                              "cpu": cpu_model(),
                              "sample": f"frames {args.warmup}..{T - 1} of stream 0 of the {args.workload} clip "
-                                       "(numpy fp64 oracle; one stream-frame per step)"},
+                                       "(numpy fp64 oracle; one stream-frame per step: a bounded sample of the "
+                                       "workload, whose streams are independent and identical in cost)"},
             "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -812,12 +822,7 @@ def main():
         "steps": steps, "warmup": args.warmup, "ms_per_step": r["total_ms"] / steps,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic (closed-form SplitMix64 video, SURVEY d2; random LSUV-scaled weights)",
-        "config": {"workload": f"{args.workload} S={S}/GPU ({wl['cfg']})", "baseline_cfg": wl["cfg"],
-                   "model": wl["model"], "streams_per_gpu": S, "frame": [net.in_h, net.in_w, 3],
-                   "input_eps": net.input_eps, "input_dilation": net.input_dilation,
-                   "inner_eps": max([L.eps for L in net.layers if L.truncates] + [0]),
-                   "l2": "flushed (256 MiB write) between timed steps",
-                   "parallelism": f"independent camera streams x{world} GPUs (no data-path collective)"},
+        "config": line_config(args, wl, net, S, world),
         "update": r.get("update"),
         "dense": r.get("dense"),
         "d9_points": points,
