@@ -122,6 +122,8 @@ struct dcnn_net {
   // graph; the input-kernel and output-copy nodes get per-call parameters (caller's frame and
   // output pointers), so no copy sits outside the graph
   cudaGraphNode_t node_input = nullptr, node_out = nullptr;
+  cudaGraphNode_t node_input1 = nullptr;     // two-pass input stage: the threshold pass
+  uint32_t* in_bits = nullptr;               // its per-row threshold bit words
   InputParams ip_cap;
   OutCopyParams oc_cap;
   cudaStream_t cap = nullptr;
@@ -364,8 +366,22 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
   ip.frame = n->frame_in; ip.P = n->P; ip.P1 = n->P1; ip.frame_idx = n->frame_idx; ip.delta = n->in_delta; ip.mask = n->in_mask;
   ip.eps = n->eps; ip.first = n->first; ip.pend = n->pend; ip.err = n->err;
   ip.cta_active = n->cta_active;
+  ip.bits = n->in_bits;
   ip.zero_stats = n->stats + 8; ip.n_zero_stats = 8 * nops;   // slot 0 (the input) is per-CTA
   ip.zero_counts = n->counts; ip.n_zero_counts = n->n_counts;
+  if (ip.bits) {                             // two-pass input stage: the threshold pass first
+    {
+      TimeScope ts(n, st, DCNN_KCLASS_INPUT);
+      launch_input_pass1(ip, n->dtype, st);
+    }
+    ++k;
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    if (cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &nd) == cudaSuccess &&
+        cs == cudaStreamCaptureStatusActive && nd == 1 && n->timing_mask == 0)
+      n->node_input1 = deps[0];
+  }
   {
     TimeScope ts(n, st, DCNN_KCLASS_INPUT);
     if (ip.radius == 0 && ip.C <= 4 && (long long)ip.S * ip.H * ip.W < (1ll << 30))   // 32-bit index math
@@ -567,6 +583,13 @@ static dcnn_status set_frame_io(dcnn_net* n, const void* frame, void* const* out
   kp.kernelParams = a_in;
   kp.extra = nullptr;
   CUDA_TRY(cudaGraphExecKernelNodeSetParams(n->exec, n->node_input, &kp));
+  if (n->node_input1) {                      // the threshold pass reads the frame too
+    cudaKernelNodeParams k1;
+    CUDA_TRY(cudaGraphKernelNodeGetParams(n->node_input1, &k1));
+    k1.kernelParams = a_in;
+    k1.extra = nullptr;
+    CUDA_TRY(cudaGraphExecKernelNodeSetParams(n->exec, n->node_input1, &k1));
+  }
   cudaKernelNodeParams ko;
   CUDA_TRY(cudaGraphKernelNodeGetParams(n->node_out, &ko));
   OutCopyParams oc = n->oc_cap;
@@ -791,7 +814,13 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   CUDA_TRY(cudaMemset(n->frame_idx, 0, S * sizeof(long long)));
 
   CUDA_TRY(cudaMemset(n->P, 0, n->frame_bytes));
-  if (n->radius > 0 && n->bookkeeper >= 0) {   // halo reads of P race with in-place updates
+  const bool two_pass = input_two_pass(n->S, n->inH, n->inW, n->inC, n->radius);
+  if (two_pass) {
+    const size_t words = (size_t)n->S * n->inH * ((n->inW + 31) / 32);
+    if ((r = dalloc(n, &n->in_bits, words * 4))) return r;
+    CUDA_TRY(cudaMemset(n->in_bits, 0, words * 4));
+  }
+  if (n->radius > 0 && n->bookkeeper >= 0 && !two_pass) {   // halo reads of P race with in-place updates
     if ((r = dalloc(n, &n->P1, n->frame_bytes))) return r;
     CUDA_TRY(cudaMemset(n->P1, 0, n->frame_bytes));
   }

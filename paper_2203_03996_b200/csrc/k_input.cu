@@ -235,7 +235,179 @@ __global__ void __launch_bounds__(256, 3) k_input_c4(InputParams p) {
   input_frame_counters(p.zero_stats, p.n_zero_stats, p.zero_counts, p.n_zero_counts, p.cta_active, nact);
 }
 
+// ---- two-pass input stage (C <= 4, dilation r >= 1): a1 at HBM speed without halo re-reads
+// Pass 1: one warp per 32-pixel row word: threshold (Z1, strict) -> one bit per pixel (ballot);
+// the first-frame flags of this frame are copied from the pending ones; non-finite inputs are
+// flagged.  Pass 2: one warp per word: Chebyshev dilation by r (Z4) of the bit words of rows
+// y - r .. y + r and words x - 1 .. x + 1 (64-bit shifts), then the emit: mask for every pixel,
+// and on the mask delta = F - P (F on a first frame) and P := F.  P is updated in place: every
+// read of P that crosses pixels (the thresholds) happened in pass 1.
+template <typename T, int C>
+__global__ void __launch_bounds__(256) k_input_bits(InputParams p) {
+  constexpr int U = 4;                            // row words per warp iteration (loads in flight)
+  pdl_trigger();
+  pdl_wait();
+  const int WW = (p.W + 31) / 32;
+  const int nw = p.S * p.H * WW;
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0)
+    for (int s = threadIdx.x; s < p.S; s += blockDim.x) p.first[s] = p.pend[s] != 0 ? 1 : 0;
+  const float eps = *p.eps;
+  const T* F = reinterpret_cast<const T*>(p.frame);
+  const T* P = reinterpret_cast<const T*>(p.P);
+  bool bad = false;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int wb = gw * U; wb < nw; wb += nwarps * U) {
+    float f[U][C], pv[U][C];
+    bool in[U], fst[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {                 // every load of the U words first
+      const int wi = wb + u;
+      const int s = wi / (p.H * WW), rem = wi - s * p.H * WW;
+      const int y = rem / WW, x = (rem - y * WW) * 32 + lane;
+      in[u] = wi < nw && x < p.W;
+      fst[u] = wi < nw && p.pend[s] != 0;
+      const long long o = in[u] ? (((long long)s * p.H + y) * p.W + x) * C : 0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        f[u][c] = in[u] ? ld(F + o + c) : 0.f;
+        pv[u][c] = (in[u] && !fst[u]) ? ld(P + o + c) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float mx = 0.f;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        bad |= in[u] && !isfinite(f[u][c]);
+        mx = fmaxf(mx, fabsf(f[u][c] - pv[u][c]));
+      }
+      const uint32_t b = __ballot_sync(0xffffffffu, in[u] && (fst[u] || eps < 0.f || mx > eps));   // Z1 strict
+      if (lane == 0 && wb + u < nw) p.bits[wb + u] = b;
+    }
+  }
+  if (bad) atomicOr(p.err, 1);
+}
+
+template <typename T, int C>
+__global__ void __launch_bounds__(256) k_input_emit(InputParams p) {
+  constexpr int U = 4;
+  pdl_trigger();
+  pdl_wait();
+  const int WW = (p.W + 31) / 32;
+  const int nw = p.S * p.H * WW;
+  const int lane = threadIdx.x & 31, r = p.radius;
+  const T* F = reinterpret_cast<const T*>(p.frame);
+  T* P = reinterpret_cast<T*>(p.P);
+  T* D = reinterpret_cast<T*>(p.delta);
+  unsigned nact = 0;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int wb = gw * U; wb < nw; wb += nwarps * U) {
+    // Chebyshev dilation is separable: OR the 2r + 1 rows first (lane l loads row y - r + l's
+    // words x - 1, x, x + 1; warp OR-reduction), then dilate the 96-bit row window once
+    uint32_t wl[U], w0[U], wr[U];
+    int ys[U], xs[U], ss[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int wi = wb + u < nw ? wb + u : nw - 1;
+      const int s = wi / (p.H * WW), rem = wi - s * p.H * WW;
+      const int y = rem / WW, xw = rem - y * WW;
+      ss[u] = s; ys[u] = y; xs[u] = xw;
+      wl[u] = w0[u] = wr[u] = 0u;
+      const uint32_t* rows = p.bits + (long long)s * p.H * WW;
+      for (int rr = lane; rr <= 2 * r; rr += 32) {
+        const int yy = y - r + rr;
+        if (yy < 0 || yy >= p.H) continue;
+        const uint32_t* rw = rows + yy * WW;
+        w0[u] |= rw[xw];
+        if (xw > 0) wl[u] |= rw[xw - 1];
+        if (xw + 1 < WW) wr[u] |= rw[xw + 1];
+      }
+    }
+    uint32_t m[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        w0[u] |= __shfl_xor_sync(0xffffffffu, w0[u], o);
+        wl[u] |= __shfl_xor_sync(0xffffffffu, wl[u], o);
+        wr[u] |= __shfl_xor_sync(0xffffffffu, wr[u], o);
+      }
+      const unsigned long long A = ((unsigned long long)wr[u] << 32) | w0[u];   // positions 0 .. 63
+      const unsigned long long B = ((unsigned long long)w0[u] << 32) | wl[u];   // positions -32 .. 31
+      unsigned long long R = 0, Lf = 0;
+      for (int k = 0; k <= r; ++k) {
+        R |= A >> k;                                // bit j: a set position in j .. j + r
+        Lf |= B << k;                               // bit 32 + j: a set position in j - r .. j
+      }
+      m[u] = (uint32_t)R | (uint32_t)(Lf >> 32);
+    }
+    // emit: loads of every active pixel first, then the stores
+    float f[U][C], pv[U][C];
+    bool v[U], fst[U];
+    long long pix[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int x = xs[u] * 32 + lane;
+      const bool ok = wb + u < nw && x < p.W;
+      v[u] = ok && ((m[u] >> lane) & 1u);
+      fst[u] = p.first[ss[u]] != 0;
+      pix[u] = ((long long)ss[u] * p.H + ys[u]) * p.W + x;
+      if (ok) p.mask[pix[u]] = v[u] ? 1 : 0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        f[u][c] = v[u] ? ld(F + pix[u] * C + c) : 0.f;
+        pv[u][c] = (v[u] && !fst[u]) ? ld(P + pix[u] * C + c) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!v[u]) continue;
+      ++nact;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        st(D + pix[u] * p.Cp + c, fst[u] ? f[u][c] : f[u][c] - pv[u][c]);   // own delta (Z4)
+        st(P + pix[u] * C + c, f[u][c]);          // P := F on the mask
+      }
+    }
+  }
+  input_frame_counters(p.zero_stats, p.n_zero_stats, p.zero_counts, p.n_zero_counts, p.cta_active, nact);
+}
+
+bool input_two_pass(int S, int H, int W, int C, int radius) {
+  static const bool off = getenv("DCNN_INPUT_ONE_PASS") != nullptr;
+  return !off && C >= 1 && C <= 4 && radius >= 1 && radius <= 16 && (long long)S * H * W * 4 < (1ll << 31);
+}
+
+static int input2_grid(const InputParams& p) {
+  const long long warps = ((long long)p.S * p.H * ((p.W + 31) / 32) + 3) / 4;   // 4 words per warp
+  const long long blocks = (warps + 7) / 8;
+  return (int)(blocks < INPUT_MAX_GRID ? blocks : INPUT_MAX_GRID);
+}
+
+void launch_input_pass1(const InputParams& p, int dtype, cudaStream_t st) {
+  auto go = [&](auto kern) { launch_k(kern, dim3(input2_grid(p)), dim3(256), 0, st, 1, p); };
+  if (dtype == 1) {
+    if (p.C == 1) go(k_input_bits<__half, 1>); else if (p.C == 2) go(k_input_bits<__half, 2>);
+    else if (p.C == 3) go(k_input_bits<__half, 3>); else go(k_input_bits<__half, 4>);
+  } else {
+    if (p.C == 1) go(k_input_bits<float, 1>); else if (p.C == 2) go(k_input_bits<float, 2>);
+    else if (p.C == 3) go(k_input_bits<float, 3>); else go(k_input_bits<float, 4>);
+  }
+}
+
 void launch_input(const InputParams& p, int dtype, cudaStream_t st) {
+  if (p.bits) {                                   // pass 2 (pass 1 was launched before)
+    auto go = [&](auto kern) { launch_k(kern, dim3(input2_grid(p)), dim3(256), 0, st, 1, p); };
+    if (dtype == 1) {
+      if (p.C == 1) go(k_input_emit<__half, 1>); else if (p.C == 2) go(k_input_emit<__half, 2>);
+      else if (p.C == 3) go(k_input_emit<__half, 3>); else go(k_input_emit<__half, 4>);
+    } else {
+      if (p.C == 1) go(k_input_emit<float, 1>); else if (p.C == 2) go(k_input_emit<float, 2>);
+      else if (p.C == 3) go(k_input_emit<float, 3>); else go(k_input_emit<float, 4>);
+    }
+    return;
+  }
   const int tiles = p.S * ((p.H + IN_TS - 1) / IN_TS) * ((p.W + IN_TS - 1) / IN_TS);
   const int grid = tiles < INPUT_MAX_GRID ? tiles : INPUT_MAX_GRID;
   if (p.C <= 4 && p.radius >= 1 && p.radius <= IN_RMAX && p.P1 && (long long)p.H * p.W * p.C < (1ll << 31) &&

@@ -34,7 +34,11 @@ struct InputParams {
   // counters only after its PDL wait, i.e. after this grid has finished
   unsigned long long* zero_stats; int n_zero_stats;
   int* zero_counts; int n_zero_counts;
+  uint32_t* bits;               // two-pass input stage (C <= 4, r >= 1): per-row threshold bit
+                                // words [S][H][ceil(W/32)]; null: single-pass kernels
 };
+bool input_two_pass(int S, int H, int W, int C, int radius);   // host: is the two-pass path used
+void launch_input_pass1(const InputParams& p, int dtype, cudaStream_t st);
 constexpr int INPUT_MAX_GRID = 148 * 16;
 void launch_input(const InputParams& p, int dtype, cudaStream_t st);
 
