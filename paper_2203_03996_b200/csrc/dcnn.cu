@@ -221,8 +221,18 @@ static bool plan_tc(Op& o, int dtype, int flags) {
   const double budget = 226 * 1024 - 69632;
   const int ntaps = o.kh * o.kw;
   const int plane = (p.HH * p.WQ * 16 + 127) / 128 * 128;
-  struct Cand { double cost; int ns, BK, tg, stages, nab, resident; };
-  Cand best = {1e30, 0, 0, 0, 0, 0, 0};
+  // swizzled halo rows (p.swz): one TMA element per pixel and channel block instead of one
+  // per 8-channel plane.  DCNN_TC_NO_SWZ: planes only; DCNN_TC_SWZ_ONLY: swizzled where possible;
+  // DCNN_TC_SWZ_PAD: row pitch padded so s * pitch is a multiple of 8 rows (pattern-aligned SBO)
+  static const bool no_swz = getenv("DCNN_TC_NO_SWZ") != nullptr;
+  static const bool swz_only = getenv("DCNN_TC_SWZ_ONLY") != nullptr;
+  static const bool swz_pad = getenv("DCNN_TC_SWZ_PAD") != nullptr;
+  static const bool old_model = getenv("DCNN_TC_MODEL_OLD") != nullptr;
+  static const double t_req = getenv("DCNN_TC_TREQ") ? atof(getenv("DCNN_TC_TREQ")) : 0.0028;
+  int WQs = p.WQ;
+  if (swz_pad) while ((s * WQs) % 8) ++WQs;
+  struct Cand { double cost; int ns, BK, tg, stages, nab, resident, swz; };
+  Cand best = {1e30, 0, 0, 0, 0, 0, 0, 0};
   // power-of-two splits first; 3, 5, 6, 7 only when none fits (e.g. 672 = 3 x 224 channels)
   for (int pass = 0; pass < 2 && best.ns == 0; ++pass)
   for (int ns = 1; ns <= max_split; ++ns) {
@@ -236,11 +246,20 @@ static bool plan_tc(Op& o, int dtype, int flags) {
     const int waves = (ntiles * ns + 147) / 148;
     const int c_thread = (Ns + 31) / 32 * 16;            // channels of an epilogue thread
     const double t_epi = 3.5 + 0.35 * std::max(0, c_thread - 32) + (ns > 1 ? 1.0 : 0.0);
-    for (int BK = 64; BK >= 16; BK /= 2) {
+    for (int BK = 64; BK >= 16; BK /= 2)
+    for (int sw = 1; sw >= 0; --sw) {
       if (o.Ci % BK) continue;
-      if (o.kh == 1 && o.kw == 1 && s == 1 && o.Ci % 64 == 0 && BK != 64) continue;   // swizzled path
-      const double a_bytes = (double)s * (BK / 8) * plane;
-      if (plane >> 4 >= (1 << 14)) continue;             // LBO field
+      const bool pw = o.kh == 1 && o.kw == 1 && s == 1 && o.Ci % 64 == 0;
+      if (pw && (BK != 64 || !sw)) continue;             // 1x1: 128-byte swizzled rows
+      if (sw && !pw && (no_swz || BK == 16)) continue;
+      if (!sw && swz_only && !pw && o.Ci % 32 == 0) continue;
+      const int swzb = sw ? 2 * BK : 0;
+      const int phase_sw = (p.HH * WQs * swzb + 1023) / 1024 * 1024;
+      const double a_bytes = sw ? (double)s * phase_sw : (double)s * (BK / 8) * plane;
+      if (!sw && plane >> 4 >= (1 << 14)) continue;      // LBO field
+      if (sw && (s * WQs * swzb) >> 4 >= (1 << 14)) continue;   // SBO field
+      // TMA elements of one halo block: one per pixel (swizzled rows) or per pixel and plane
+      const double req = sw ? (double)s * p.HH * WQs : (double)s * p.HH * p.WQ * (BK / 8);
       const int ncb = o.Ci / BK;
       const double m_cb = ntaps * (BK / 16) * t_mma;     // MMAs of one halo block
       const double t_mmas = ncb * m_cb;
@@ -258,7 +277,7 @@ static bool plan_tc(Op& o, int dtype, int flags) {
             // each; 1188 for 16 channels of a 3x3 s2 tile), so keep >= 2 blocks in flight
             // (YOLOv5s 40x40x256 s2: K loop 79 -> 51 us, profiles/r02_trace_s2_convs_nab.txt;
             // YOLOv5s S = 8 +2.3 %; at S = 1 the other plans win by 2 %, profiles/r02_ab.md)
-            if (s == 2 && nab == 2 && ncb >= 3 && o.tS >= 4 && !s2_nab2) continue;
+            if (!sw && s == 2 && nab == 2 && ncb >= 3 && o.tS >= 4 && !s2_nab2) continue;
             double wb;
             int stages;
             if (resident) {
@@ -271,7 +290,9 @@ static bool plan_tc(Op& o, int dtype, int flags) {
               wb = stages * b_bytes;
             }
             if (nab * a_bytes + wb > budget) continue;
-            const double t_halo = ncb * std::max(m_cb, 1.5 / (nab - 1));
+            const double t_blk = req * t_req;
+            const double t_halo = old_model ? ncb * std::max(m_cb, 1.5 / (nab - 1))
+                                            : ncb * std::max(m_cb, std::max(t_blk, (1.0 + t_blk) / (nab - 1)));
             double t_w = 0.0;
             if (!resident) {
               const double copy = 0.55 + b_bytes / 40e3;
@@ -280,7 +301,7 @@ static bool plan_tc(Op& o, int dtype, int flags) {
             }
             const double t_tile = std::max(std::max(t_halo, t_w), t_mmas);
             const double cost = t_tile + t_epi + (waves - 1) * std::max(t_tile, t_epi);
-            if (cost < best.cost - 1e-9) best = {cost, ns, BK, tg, stages, nab, resident};
+            if (cost < best.cost - 1e-9) best = {cost, ns, BK, tg, stages, nab, resident, swzb};
           }
           if (resident) break;                            // resident: largest tg with <= 16 steps
         }
@@ -288,8 +309,9 @@ static bool plan_tc(Op& o, int dtype, int flags) {
     }
   }
   if (best.ns == 0) return false;
-  static const bool no_sw = getenv("DCNN_TC_NO_SW128") != nullptr;
-  p.sw128 = (!no_sw && o.kh == 1 && o.kw == 1 && s == 1 && best.BK == 64) ? 1 : 0;
+  p.swz = best.swz;
+  p.sw128 = p.swz == 128;
+  p.swz_bofs = getenv("DCNN_TC_SWZ_BOFS") ? atoi(getenv("DCNN_TC_SWZ_BOFS")) : 0;
 
   p.nsplit = best.ns;
   p.Ns = p.Np / best.ns;
@@ -297,12 +319,23 @@ static bool plan_tc(Op& o, int dtype, int flags) {
   p.ncb = o.Ci / best.BK;
   p.plane = plane;
   p.phase_bytes = (best.BK / 8) * plane;
+  if (p.swz) {
+    p.WQ = WQs;
+    p.phase_bytes = (p.HH * WQs * p.swz + 1023) / 1024 * 1024;
+  }
   p.a_bytes = s * p.phase_bytes;
   p.tg = best.tg;
   p.b_bytes = best.tg * p.Ns * best.BK * 2;
   p.stages = best.stages;
   p.n_abuf = best.nab;
   p.resident = best.resident;
+  // two epilogue groups on alternate tiles where a cluster walks >= 2 tiles
+  // (DCNN_TC_EGRP = 0 / 1 forces it off / on)
+  {
+    static const int egrp_env = getenv("DCNN_TC_EGRP") ? atoi(getenv("DCNN_TC_EGRP")) : -1;
+    const int ncl = std::max(1, std::min(ntiles, 148 / p.nsplit));
+    p.egrp = egrp_env >= 0 ? egrp_env : (ntiles >= 2 * ncl ? 1 : 0);
+  }
   p.n_acc = 2;
   p.acc_stride = (p.Ns + 31) / 32 * 32;
   int tc = 32;
@@ -955,7 +988,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
           // (only where an epilogue thread holds > 32 channels, i.e. Ns > 64: with fewer, the
           // single pass that stages both outcomes in shared memory writes fewer bytes)
           static const bool no_dbl = getenv("DCNN_TC_NO_DBL") != nullptr;
-          if (!no_dbl && o.out_slot < 0 && p.Ns > 64) {
+          if (!no_dbl && o.out_slot < 0 && p.Ns > (p.egrp ? 32 : 64)) {
             if ((r = dalloc(n, &p.xA2, px * o.ld * n->cesz))) return r;
             CUDA_TRY(cudaMemset(p.xA2, 0, px * o.ld * n->cesz));
           }
@@ -975,16 +1008,18 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
           const cuuint64_t gdim[4] = {(cuuint64_t)o.Ci, (cuuint64_t)o.tWi, (cuuint64_t)o.tHi, (cuuint64_t)o.tS};
           const cuuint64_t gstr[3] = {(cuuint64_t)o.Ci * 2, (cuuint64_t)o.tWi * o.Ci * 2,
                                       (cuuint64_t)o.tHi * o.tWi * o.Ci * 2};
-          const cuuint32_t box[4] = {p.sw128 ? 64u : 8u, (cuuint32_t)(o.stride * p.WQ), (cuuint32_t)p.HH, 1};
+          const cuuint32_t box[4] = {p.swz ? (cuuint32_t)p.BK : 8u, (cuuint32_t)(o.stride * p.WQ), (cuuint32_t)p.HH, 1};
           const cuuint32_t es[4] = {1, (cuuint32_t)o.stride, 1, 1};
           CUresult cr = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, src, gdim, gstr, box, es,
                                CU_TENSOR_MAP_INTERLEAVE_NONE,
-                               p.sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                               p.swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : p.swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                               : p.swz == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
           if (cr != CUDA_SUCCESS) return fail(DCNN_ERR_CUDA, "conv " + std::to_string(i) + ": tensor map encode failed");
         }
         const int ncl = std::max(1, std::min(o.tS * o.nty * o.ntx, 148 / p.nsplit));
         o.grid_tc = ncl * p.nsplit;
+
         // a2 as a separate compaction kernel when the CTAs' scouts would otherwise walk many
         // (mostly empty) tiles each: more than two tiles per cluster
         o.scan = !force_fused && o.tS * o.nty * o.ntx > 2 * ncl;
@@ -992,10 +1027,10 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         if (show_plan)
           fprintf(stderr,
                   "[dcnn plan] op %d %dx%dx%d->%dx%dx%d k%d s%d: tiles %d nsplit %d Ns %d BK %d ncb %d tg %d steps %d "
-                  "stages %d resident %d halo_bufs %d a_bytes %d b_bytes %d smem %zu grid %d sw128 %d\n",
+                  "stages %d resident %d halo_bufs %d a_bytes %d b_bytes %d smem %zu grid %d swz %d egrp %d\n",
                   i, o.Hi, o.Wi, o.Ci, o.H, o.W, o.C, o.kh, o.stride, o.tS * o.nty * o.ntx, p.nsplit, p.Ns, p.BK,
                   p.ncb, p.tg, p.ncb * (o.kh * o.kw / p.tg), p.stages, p.resident, p.n_abuf, p.a_bytes, p.b_bytes,
-                  conv_tc_smem(p), o.grid_tc, p.sw128);
+                  conv_tc_smem(p), o.grid_tc, p.swz, p.egrp);
       }
     }
     if (o.kind == DCNN_OP_CONV) {

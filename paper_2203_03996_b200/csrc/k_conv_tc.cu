@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&acc_full[i], 1);
-      tc::mbar_init(&acc_empty[i], 256);
+      tc::mbar_init(&acc_empty[i], p.egrp ? 128 : 256);
       tc::mbar_init(&xch[i], nsplit);
     }
     for (int i = 0; i < TC_NI; ++i) {
@@ -206,7 +206,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     for (int t = lane; t < ntaps; t += 32) {
       const int ky = t / p.kw, kx = t - (t / p.kw) * p.kw;
       const int xo = kx * p.dil;
-      tapoff[t] = (uint32_t)((xo % p.stride) * p.phase_bytes + ((ky * p.dil) * p.WQ + xo / p.stride) * 16);
+      tapoff[t] = (uint32_t)((xo % p.stride) * p.phase_bytes +
+                             ((ky * p.dil) * p.WQ + xo / p.stride) * (p.swz ? p.swz : 16));
     }
   }
   tc::tc_fence_before();
@@ -385,10 +386,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       for (int px = TC_DBG(8) ? npx : lt; px < npx; px += 32) {   // dbg 8: no zero pass (trace build, timing only)
         const int iy = pg_iy0 + hy, ix = pg_ix0 + hx;
         if (!hm[px] && iy >= 0 && iy < p.H && ix >= 0 && ix < p.W) {
-          if (p.sw128) {                       // the pixel's whole 128-B row (swizzle permutes within it)
-            unsigned char* d = A + px * 128;
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch) *reinterpret_cast<uint4*>(d + ch * 16) = make_uint4(0u, 0u, 0u, 0u);
+          if (p.swz) {                         // the pixel's whole swz-byte row (swizzle permutes within it)
+            unsigned char* d = A + (hx & lgs) * p.phase_bytes + (hy * p.WQ + (hx >> lgs)) * p.swz;
+            for (int ch = 0; ch < p.swz; ch += 16) *reinterpret_cast<uint4*>(d + ch) = make_uint4(0u, 0u, 0u, 0u);
           } else {
             unsigned char* d = A + (hx & lgs) * p.phase_bytes + (hy * p.WQ + (hx >> lgs)) * 16;
             for (int ch = 0; ch < nch; ++ch)
@@ -412,8 +412,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         if (TC_DBG(16)) { tc::mbar_arrive(&a_tma[b]); return; }   // dbg 16: no halo copies (trace build)
         tc::mbar_arrive_expect_tx(&a_tma[b], gbytes);
         const uint32_t A = tc::smem_u32(smem + L.a0 + b * p.a_bytes);
-        if (p.sw128) {                         // one box: 64 channels x 8 columns x 16 rows, swizzled
-          tma_load_4d(A, &p.tmap, cb * p.BK, ix0, iy0, s, &a_tma[b]);
+        if (p.swz) {                           // one box per stride phase: BK channels x WQ x HH, swizzled
+#pragma unroll 1
+          for (int ph = 0; ph < p.stride; ++ph)
+            tma_load_4d(A + ph * p.phase_bytes, &p.tmap, cb * p.BK, ix0 + ph, iy0, s, &a_tma[b]);
           return;
         }
         // one box of 8 channels x (columns of one stride phase) x halo rows per plane
@@ -495,7 +497,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   } else if (warp == 10) {
     // ---------------------------------------------------------------- MMA issuer
     // warp-uniform loop; descriptors live in uniform registers, one elected lane issues
-    const uint32_t sbo_a = (uint32_t)(p.stride * p.WQ * 16);   // next output row = stride halo rows
+    const uint32_t sbo_a = (uint32_t)(p.stride * p.WQ * (p.swz ? p.swz : 16));   // next output row = stride halo rows
     const uint32_t lbo_b = (uint32_t)(p.Ns * 16);
     const uint32_t idesc = tc::idesc_f16(128, p.Ns);
     const uint64_t a_step = (uint64_t)((2 * p.plane) >> 4), b_step = (uint64_t)(2 * p.Ns);
@@ -532,9 +534,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             // all MMAs of tg taps x BK/16 K-steps against one weight step
             uint32_t accum = (cb | g) != 0;
             for (int t = 0; t < p.tg; ++t) {
-              uint64_t ad = p.sw128 ? tc::smem_desc_sw128(abase, 1024)
-                                    : tc::smem_desc(abase + tapoff[g * p.tg + t], p.plane, sbo_a);
-              const uint64_t a_inc = p.sw128 ? 2 : a_step;   // K = 16: +32 B inside the swizzled row
+              const uint32_t aaddr = abase + tapoff[g * p.tg + t];
+              uint64_t ad = p.swz ? tc::smem_desc_swz(aaddr, sbo_a, p.swz, p.swz_bofs)
+                                  : tc::smem_desc(aaddr, p.plane, sbo_a);
+              const uint64_t a_inc = p.swz ? 2 : a_step;     // K = 16: +32 B inside the swizzled row
               uint64_t bd = tc::smem_desc(bbase + (uint32_t)(t * p.Ns * p.BK * 2), lbo_b, 128);
               for (int kc = 0; kc < nk; ++kc) {
                 tc::mma_f16(dbase, ad, bd, idesc, accum);
@@ -567,12 +570,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     // writes caches, delta and output.  The first 32 channels of each half keep d in
     // registers between the passes, and their cache rows are loaded while the MMAs run.
     const Epi& e = p.ep;
-    const int q4 = warp & 3, half = warp >> 2;
+    // p.egrp: the two groups of 4 warps take alternate tiles (group g = accumulator g) and
+    // each owns ALL of the CTA's channels, so two tiles' epilogues (cache round trips, norm,
+    // flush) overlap; otherwise both groups split one tile's channels (halves).
+    const int q4 = warp & 3, grp = warp >> 2, half = p.egrp ? 0 : grp;
+    const bool lead = p.egrp || half == 0;     // this thread owns its pixel's mask / state bytes
     const int m = q4 * 32 + lane;              // output pixel of the tile = TMEM lane
     const int Cg = e.C;                        // channels of the output rows (pitch)
     const int cb0 = rank * p.Ns;               // this CTA's first output channel
     const int Ccta = min(p.Ns, Cg - cb0);      // this CTA's channels
-    const int CH = ((Ccta + 31) / 32) * 16;    // channels of half 0 (multiple of 16)
+    const int CH = p.egrp ? Ccta : ((Ccta + 31) / 32) * 16;   // channels of half 0 (multiple of 16)
     const int c_lo = half ? CH : 0;            // my first channel (relative to cb0)
     const int C = half ? max(0, Ccta - CH) : min(CH, Ccta);   // my channel count
     const bool vec = (Cg % 8) == 0;
@@ -589,6 +596,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       const bool mcb = tile >= 0 && ((info[slot].bits[q4] >> lane) & 1u);   // m_conv of my pixel
       tc::mbar_arrive(&info_empty[slot]);
       if (tile < 0) break;
+      if (p.egrp && (v & 1) != grp) { ++u; continue; }   // the other group's tile
       const int s = tile / (p.nty * p.ntx);
       const int ty = (tile / p.ntx) % p.nty, tx = tile % p.ntx;
       const int oy = ty * 16 + (m >> 3), ox = tx * 8 + (m & 7);
@@ -721,13 +729,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       // the cluster (DSMEM exchange)
       auto norm_combine = [&](float mx) -> float {
         const int xb = u & 1;
-        pm2[xb * 256 + half * 128 + m] = mx;
-        tc::named_bar_sync(2, 256);
-        mx = fmaxf(pm2[xb * 256 + m], pm2[xb * 256 + 128 + m]);
+        if (!p.egrp) {
+          pm2[xb * 256 + half * 128 + m] = mx;
+          tc::named_bar_sync(2, 256);
+          mx = fmaxf(pm2[xb * 256 + m], pm2[xb * 256 + 128 + m]);
+        }
         if (nsplit > 1) {
           if (half == 0) pmax[xb * 128 + m] = mx;
-          tc::named_bar_sync(2, 256);
-          if (tid == 0) {
+          if (p.egrp) tc::named_bar_sync(2 + grp, 128);
+          else tc::named_bar_sync(2, 256);
+          if (tid == (p.egrp ? grp * 128 : 0)) {
             const uint32_t local = tc::smem_u32(&xch[xb]);
             for (int r = 0; r < nsplit; ++r) tc::mbar_arrive_remote(tc::mapa(local, (uint32_t)r));
           }
@@ -918,16 +929,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         }
       }
       TCTR(tid == 0 && u == 0, 17);
-      if (inb && rank == 0 && half == 0) e.mask[pix] = upd ? 1 : 0;   // final mask of every tile pixel
+      if (inb && rank == 0 && lead) e.mask[pix] = upd ? 1 : 0;   // final mask of every tile pixel
       // pending-residual flag: written by one thread per pixel after every CTA of the cluster
       // and both halves have read it (they all passed the max-norm exchange)
       if (dbl) {
         // updated: the other x^A buffer becomes current, x^T = 0; truncated: x^T pending
-        if (act && rank == 0 && half == 0) p.tflag[pix] = upd ? (uint8_t)((fl & 2) ^ 2) : (uint8_t)((fl & 2) | 1);
-      } else if (trunc && p.tflag && act && rank == 0 && half == 0 && upd == tpend) {
+        if (act && rank == 0 && lead) p.tflag[pix] = upd ? (uint8_t)((fl & 2) ^ 2) : (uint8_t)((fl & 2) | 1);
+      } else if (trunc && p.tflag && act && rank == 0 && lead && upd == tpend) {
         p.tflag[pix] = upd ? 0 : 1;
       }
-      nact += (upd && rank == 0 && half == 0) ? 1 : 0;
+      nact += (upd && rank == 0 && lead) ? 1 : 0;
       TCTR(tid == 0 && u == 0, 12);
       tc::tc_fence_before();
       tc::mbar_arrive(&acc_empty[acc]);

@@ -109,8 +109,13 @@ struct ConvTCParams {
   int n_abuf;                   // halo buffers (2..4)
   int resident;                 // 1: all weight steps of the CTA stay in smem (stages = steps)
   int tg;                       // taps per weight stage (divides kh*kw)
-  int sw128;                    // 1x1 s1 convs, BK = 64: halo rows of 128 B (one pixel's channel
-                                // block) in the 128-byte-swizzled K-major layout, one TMA box per block
+  int sw128;                    // swz == 128 (kept for the plan printout / 1x1 fast checks)
+  int swz;                      // 0: 8-channel planes (16-byte TMA elements).  32 / 64 / 128: halo
+                                // rows of swz bytes (one pixel's BK = swz / 2 channels) in the
+                                // swz-byte-swizzled K-major layout, one TMA box per stride phase
+                                // and channel block; WQ is then the row pitch (pixels per halo row)
+  int egrp;                     // 1: the two epilogue warp groups take alternate tiles, all channels each
+  int swz_bofs;                 // descriptor base-offset mode of shifted tap starts (see tc.cuh)
   int n_acc, acc_stride;        // TMEM accumulators and their column stride
   int tmem_cols;
   int nsplit, Ns;               // output channels split over a cluster of nsplit CTAs (Ns each)

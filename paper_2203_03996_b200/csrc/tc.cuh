@@ -194,6 +194,21 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t sbo
   return d;
 }
 
+// K-major, swz-byte swizzle (swz = 32 / 64 / 128: layout type 6 / 4 / 2 at bits [61,64)),
+// 8 rows of swz bytes per atom, SBO = byte distance of consecutive 8-row groups, LBO unused.
+// A start address inside a pattern repeat (a tap's shifted halo row) may carry the matrix
+// base offset (bits [49,52)) = (addr >> 7) & 7 when bofs is set.
+__device__ __forceinline__ uint64_t smem_desc_swz(uint32_t saddr, uint32_t sbo, int swz, int bofs) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  if (bofs) d |= (uint64_t)((saddr >> 7) & 7) << 49;
+  d |= (uint64_t)(swz == 128 ? 2 : swz == 64 ? 4 : 6) << 61;
+  return d;
+}
+
 // Instruction descriptor kind::f16: A,B fp16 (format 0), D fp32 (c_format=1 at bit 4),
 // both K-major, N>>3 at bit 17, M>>4 at bit 24.
 __host__ __device__ __forceinline__ uint32_t idesc_f16(int M, int N) {
