@@ -51,6 +51,11 @@
 namespace dcnn {
 
 constexpr int TC_THREADS = 384;
+#ifndef DCNN_TC_ROLE_REGS
+#define DCNN_TC_ROLE_REGS 96
+#define DCNN_TC_EPI_REGS 200
+#endif
+constexpr int TC_ROLE_REGS = DCNN_TC_ROLE_REGS, TC_EPI_REGS = DCNN_TC_EPI_REGS;   // 4 x R + 8 x E <= 12 x 168
 constexpr int TC_NI = 4;              // tile-slot ring depth (scouts run ahead by up to 4 tiles)
 constexpr int TC_HMASK_BYTES = 1024;  // halo update mask of one tile (u8)
 constexpr int TC_STAGE_WARP = 3 * 32 * 80;  // per-epilogue-warp row staging: 3 areas x 32 px x (64 + 16) B
@@ -236,6 +241,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   TCTR(threadIdx.x == 0, 2);
   const int count = p.fused ? p.ntiles : *p.count;
   auto tile_of = [&](int ti) { return p.fused ? ti : p.list[ti]; };
+  // register rebalancing between the warpgroups (setmaxnreg, executed uniformly by each
+  // warpgroup): the role warps (8-11: loader, weight producer, MMA issuer, scout) need few
+  // registers, the epilogue warpgroups (0-7) are at the 168-register cap of 384 threads
+  // (rematerialised index math, spills) and get the difference
+  if (warp >= 8) {
+#ifndef DCNN_NO_SETMAXNREG
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(TC_ROLE_REGS));
+#endif
 
   if (warp == 11) {
     // ---------------------------------------------------------------- scout (one warp)
@@ -562,7 +575,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       TCTR(lane == 0 && u == 0, 9);
       ++u;
     }
+  }
   } else {
+#ifndef DCNN_NO_SETMAXNREG
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(TC_EPI_REGS));
+#endif
+  {
     // ---------------------------------------------------------------- epilogue (warps 0-7)
     // thread = (TMEM lane = output pixel, half of the CTA's output channels).  Pass 1 forms
     // s = x^A + x^T + dx and d = f(s) - f(x^A) (Eqs. 5-6) and the pixel's max-norm; the two
@@ -947,6 +965,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     // one atomic per warp
     unsigned n = (unsigned)warp_sum((int)nact);
     warp_count_flush(e.n_active, lane, n);
+  }
   }
   TCTR(threadIdx.x == 0, 13);
   if (nsplit > 1) tc::cluster_sync_all();     // partners may still read our smem
