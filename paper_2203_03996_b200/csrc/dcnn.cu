@@ -104,6 +104,11 @@ struct dcnn_net {
   void* P = nullptr;
   void* P1 = nullptr;               // second P buffer when the input mask is dilated (r > 0)
   void* in_delta = nullptr;
+  // space-to-depth stem (k_input.cu): the input's only consumer, an even-k stride-2 conv on
+  // C <= 4 channels, runs as a (k/2)-tap stride-1 conv over 2x2 pixel blocks of 16 channels
+  int s2d_op = -1, s2d_k = 0;
+  void* in_delta2 = nullptr;        // [S,H/2,W/2,16] block deltas
+  uint8_t* in_mask2 = nullptr;      // [S,H/2,W/2] block mask
   uint8_t* in_mask = nullptr;
   uint8_t* first = nullptr;         // [S] this frame's first-frame flags (written by the input kernel)
   uint8_t* pend = nullptr;          // [S] first frame pending (create / dcnn_reset)
@@ -432,9 +437,18 @@ static void enqueue_frame(dcnn_net* n, cudaStream_t st, int* kcount) {
       n->ip_cap = ip;
     }
   }
+  if (n->s2d_op >= 0) {                      // block view of the input for the space-to-depth stem
+    S2dParams sp;
+    sp.S = n->S; sp.H = n->inH; sp.W = n->inW; sp.C = n->inC;
+    sp.delta = n->in_delta; sp.mask = n->in_mask; sp.delta2 = n->in_delta2; sp.mask2 = n->in_mask2;
+    TimeScope ts(n, st, DCNN_KCLASS_INPUT);
+    launch_input_s2d(sp, st);
+    ++k;
+  }
   if (!n->aux.empty()) cudaEventRecord(n->ev_input, st);
-  auto src_delta = [&](int j) -> const void* { return j < 0 ? n->in_delta : n->ops[j].delta; };
-  auto src_mask = [&](int j) -> const uint8_t* { return j < 0 ? n->in_mask : n->ops[j].mask; };
+  // (the space-to-depth stem is the input's only consumer)
+  auto src_delta = [&](int j) -> const void* { return j < 0 ? (n->s2d_op >= 0 ? n->in_delta2 : n->in_delta) : n->ops[j].delta; };
+  auto src_mask = [&](int j) -> const uint8_t* { return j < 0 ? (n->s2d_op >= 0 ? n->in_mask2 : n->in_mask) : n->ops[j].mask; };
   // Independent branches (HRNet's parallel resolutions, YOLOv5s' C3 paths) are
   // captured on separate streams so the graph runs them concurrently: an op continues
   // the stream of a producer whose chain it extends, otherwise takes the least recently
@@ -806,6 +820,26 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
     o.Ci_real = o.Ci;
     if (o.in[0] < 0) o.Ci = n->inCp;
   }
+  // space-to-depth stem: sum_{ky,kx,c} dx[2oy-p+ky, 2ox-p+kx, c] w[ky,kx,c] regrouped over
+  // 2x2 blocks (ky = 2ky'+dy, kx = 2kx'+dx) is a (k/2)x(k/2) stride-1 conv with pad p/2 over
+  // block channels (dy*2+dx)*C + c -- the same sum (Eq. 1), 4x fewer K steps (YOLOv5s 6x6 s2 stem)
+  if (n->inCp == 16 && n->inC <= 4 && n->inH % 2 == 0 && n->inW % 2 == 0 && !getenv("DCNN_NO_S2D") &&
+      !(n->flags & (DCNN_FLAG_HYBRID_DISPATCH | DCNN_FLAG_PER_PIXEL))) {
+    int cons = -1, ncons = 0;
+    for (int i = 0; i < L; ++i)
+      for (int j = 0; j < n->ops[i].n_in; ++j)
+        if (n->ops[i].in[j] < 0) { cons = i; ++ncons; }
+    if (ncons == 1) {
+      Op& o = n->ops[cons];
+      if (o.kind == DCNN_OP_CONV && o.kh == o.kw && o.kh % 2 == 0 && o.stride == 2 && o.pad % 2 == 0 &&
+          o.dil == 1 && o.groups == 1) {
+        n->s2d_op = cons;
+        n->s2d_k = o.kh;
+        o.Hi = n->inH / 2; o.Wi = n->inW / 2; o.Ci = o.Ci_real = o.Cin[0] = 16;
+        o.kh = o.kw = o.kh / 2; o.stride = 1; o.pad /= 2;
+      }
+    }
+  }
   if (d->n_outputs > MAX_OUT) return fail(DCNN_ERR_UNSUPPORTED, "at most 16 output ops");
   for (int k = 0; k < d->n_outputs; ++k) {
     int j = d->output_ops[k];
@@ -824,6 +858,12 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
   if ((r = dalloc(n, &n->in_delta, in_px * n->inCp * es))) return r;
   CUDA_TRY(cudaMemset(n->in_delta, 0, in_px * n->inCp * es));
   if ((r = dalloc(n, &n->in_mask, in_px))) return r;
+  if (n->s2d_op >= 0) {
+    if ((r = dalloc(n, &n->in_delta2, in_px / 4 * 16 * es))) return r;
+    CUDA_TRY(cudaMemset(n->in_delta2, 0, in_px / 4 * 16 * es));
+    if ((r = dalloc(n, &n->in_mask2, in_px / 4))) return r;
+    CUDA_TRY(cudaMemset(n->in_mask2, 0, in_px / 4));
+  }
   if ((r = dalloc(n, &n->first, S))) return r;
   if ((r = dalloc(n, &n->pend, S))) return r;
   if ((r = dalloc(n, &n->frame_idx, S * sizeof(long long)))) return r;
@@ -917,6 +957,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
       if (!o.tc && o.ld != o.C) return fail(DCNN_ERR_UNSUPPORTED, "conv " + std::to_string(i) + ": padded head without tensor-core plan");
       if (o.tc) { o.TH = 16; o.TW = 8; }
       o.K = o.kh * o.kw * (o.Ci_real / o.groups);
+      if (i == n->s2d_op) o.K = n->s2d_k * n->s2d_k * n->inC;   // algorithmic MACs per output pixel
       o.nty = (o.tH + o.TH - 1) / o.TH;
       o.ntx = (o.tW + o.TW - 1) / o.TW;
       const int ntiles = o.tS * o.nty * o.ntx;
@@ -929,13 +970,26 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
       // weights: OHWI [Co][kh][kw][Ci/g] -> [kh*kw][Ci][Cp] fp32, groups expanded densely,
       // values rounded to the storage dtype (the method's weights are in dtype).
       const int Cg = o.Ci_real / o.groups, Og = o.C / o.groups;
+      const float* wsrc = ld.weight;
+      std::vector<float> w2;                                // space-to-depth stem: block weights
+      if (i == n->s2d_op) {
+        const int k = n->s2d_k, k2 = o.kh, C0 = n->inC;
+        w2.assign((size_t)o.C * k2 * k2 * 16, 0.f);
+        for (int co = 0; co < o.C; ++co)
+          for (int ky = 0; ky < k; ++ky)
+            for (int kx = 0; kx < k; ++kx)
+              for (int c = 0; c < C0; ++c)
+                w2[(((size_t)co * k2 + ky / 2) * k2 + kx / 2) * 16 + ((ky & 1) * 2 + (kx & 1)) * C0 + c] =
+                    ld.weight[(((size_t)co * k + ky) * k + kx) * C0 + c];
+        wsrc = w2.data();
+      }
       std::vector<float> wt((size_t)o.kh * o.kw * o.Ci * o.Cp, 0.f);
       for (int co = 0; co < o.C; ++co) {
         const int g = co / Og;
         for (int ky = 0; ky < o.kh; ++ky)
           for (int kx = 0; kx < o.kw; ++kx)
             for (int ci = 0; ci < Cg; ++ci) {
-              float v = ld.weight[(((size_t)co * o.kh + ky) * o.kw + kx) * Cg + ci];
+              float v = wsrc[(((size_t)co * o.kh + ky) * o.kw + kx) * Cg + ci];
               if (n->dtype == DCNN_F16) v = __half2float(__float2half_rn(v));
               wt[((size_t)(ky * o.kw + kx) * o.Ci + g * Cg + ci) * o.Cp + co] = v;
             }
@@ -1004,7 +1058,7 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
             if (!f || q != cudaDriverEntryPointSuccess) return fail(DCNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
             encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
           }
-          void* src = o.in[0] < 0 ? n->in_delta : n->ops[o.in[0]].delta;
+          void* src = o.in[0] < 0 ? (n->s2d_op >= 0 ? n->in_delta2 : n->in_delta) : n->ops[o.in[0]].delta;
           const cuuint64_t gdim[4] = {(cuuint64_t)o.Ci, (cuuint64_t)o.tWi, (cuuint64_t)o.tHi, (cuuint64_t)o.tS};
           const cuuint64_t gstr[3] = {(cuuint64_t)o.Ci * 2, (cuuint64_t)o.tWi * o.Ci * 2,
                                       (cuuint64_t)o.tHi * o.tWi * o.Ci * 2};

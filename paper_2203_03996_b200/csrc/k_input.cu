@@ -11,6 +11,7 @@
 // emits the block.  The only HBM traffic is F and P (read), delta and P
 // (written on active pixels) and the u8 mask.
 #include "kernels.h"
+#include <algorithm>
 
 namespace dcnn {
 
@@ -424,6 +425,60 @@ void launch_input(const InputParams& p, int dtype, cudaStream_t st) {
   }
   if (dtype == 1) launch_k(k_input<__half>, dim3(grid), dim3(256), 0, st, 1, p);
   else launch_k(k_input<float>, dim3(grid), dim3(256), 0, st, 1, p);
+}
+
+// ---------------------------------------------------------------- space-to-depth view of the input
+// For a stem conv of even k x k, stride 2, even pad on a C <= 4 channel input (YOLOv5s: 6x6 s2,
+// 3 channels) the same sum is a (k/2) x (k/2) stride-1 conv over 2x2 pixel blocks of 4C <= 16
+// channels (block channel (dy*2 + dx)*C + c = pixel (2by + dy, 2bx + dx) channel c): 4x fewer
+// K steps and halo pixels than the stride-2 conv over 16-channel-padded pixels, whose K is 81 %
+// zero padding.  A block is active iff one of its 4 pixels is (the receptive field of an output
+// pixel is a union of whole blocks, so m_conv is unchanged); an active block carries the deltas
+// of its active pixels and zeros for the others (the conv must not see stale deltas).  Inactive
+// blocks are not written (the conv never reads them: their mask bytes are 0).
+template <int C>
+__global__ void __launch_bounds__(256) k_input_s2d(S2dParams p) {
+  pdl_trigger();
+  pdl_wait();
+  const int Hb = p.H >> 1, Wb = p.W >> 1;
+  const long long nb = (long long)p.S * Hb * Wb;
+  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nb; b += (long long)gridDim.x * blockDim.x) {
+    const long long s = b / ((long long)Hb * Wb);
+    const int r = (int)(b - s * Hb * Wb), by = r / Wb, bx = r - by * Wb;
+    const long long p0 = (s * p.H + 2 * by) * p.W + 2 * bx;            // pixel (2by, 2bx)
+    const uint16_t m0 = *reinterpret_cast<const uint16_t*>(p.mask + p0);
+    const uint16_t m1 = *reinterpret_cast<const uint16_t*>(p.mask + p0 + p.W);
+    const bool act = (m0 | m1) != 0;
+    p.mask2[b] = act ? 1 : 0;
+    if (!act) continue;
+    const bool pm[4] = {(m0 & 0xffu) != 0, (m0 >> 8) != 0, (m1 & 0xffu) != 0, (m1 >> 8) != 0};
+    const long long px[4] = {p0, p0 + 1, p0 + p.W, p0 + p.W + 1};
+    uint2 v[4];                                // channels 0..3 of each pixel's delta row (Cp = 16)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      v[k] = pm[k] ? *reinterpret_cast<const uint2*>(reinterpret_cast<const __half*>(p.delta) + px[k] * 16)
+                   : make_uint2(0u, 0u);
+    __half o[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) o[k] = __float2half(0.f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const __half* h = reinterpret_cast<const __half*>(&v[k]);
+#pragma unroll
+      for (int c = 0; c < C; ++c) o[k * C + c] = h[c];
+    }
+    uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.delta2) + b * 16);
+    d[0] = *reinterpret_cast<const uint4*>(&o[0]);
+    d[1] = *reinterpret_cast<const uint4*>(&o[8]);
+  }
+}
+
+void launch_input_s2d(const S2dParams& p, cudaStream_t st) {
+  const long long nb = (long long)p.S * (p.H / 2) * (p.W / 2);
+  const int grid = (int)std::min<long long>((nb + 255) / 256, 148 * 16);
+  auto go = [&](auto kern) { launch_k(kern, dim3(grid), dim3(256), 0, st, 1, p); };
+  if (p.C == 1) go(k_input_s2d<1>); else if (p.C == 2) go(k_input_s2d<2>);
+  else if (p.C == 3) go(k_input_s2d<3>); else go(k_input_s2d<4>);
 }
 
 }  // namespace dcnn

@@ -38,6 +38,14 @@ struct InputParams {
                                 // words [S][H][ceil(W/32)]; null: single-pass kernels
 };
 bool input_two_pass(int S, int H, int W, int C, int radius);   // host: is the two-pass path used
+struct S2dParams {              // space-to-depth view of the input delta for an even-k stride-2 stem
+  int S, H, W, C;               // input pixels (H, W even), channels (<= 4)
+  const void* delta;            // [S,H,W,16] fp16 input delta (active pixels written)
+  const uint8_t* mask;          // [S,H,W] input mask
+  void* delta2;                 // [S,H/2,W/2,16] fp16 block deltas (active blocks written)
+  uint8_t* mask2;               // [S,H/2,W/2] block mask
+};
+void launch_input_s2d(const S2dParams& p, cudaStream_t st);
 void launch_input_pass1(const InputParams& p, int dtype, cudaStream_t st);
 constexpr int INPUT_MAX_GRID = 148 * 16;
 void launch_input(const InputParams& p, int dtype, cudaStream_t st);
