@@ -665,10 +665,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       };
       // fill SA / ST with the x^A / x^T rows of the pixels in pm: every global load of both
       // areas is issued before the first shared store (one round trip, not eight)
-      auto stage_fill2 = [&](const __half* baseA, const __half* baseT, int n16, uint32_t pm, uint32_t pmt,
-                             const __half* baseA1 = nullptr, uint32_t sel = 0u) {
+      // (split in two so the single-pass epilogue can keep the next slice's loads in flight
+      // while it computes and flushes the current one)
+      auto fill_issue = [&](const __half* baseA, const __half* baseT, int n16, uint32_t pm, uint32_t pmt,
+                            const __half* baseA1, uint32_t sel, uint4 (&va)[4], uint4 (&vt)[4]) {
         const int lg = n16 > 2 ? 2 : n16 - 1, lp = 1 << lg;
-        uint4 va[4], vt[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int pl = (i << (5 - lg)) + (lane >> lg), c = lane & (lp - 1);
@@ -677,6 +678,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           if (i < lp && c < n16 && ((pm >> pl) & 1u)) va[i] = *reinterpret_cast<const uint4*>(bA + off);
           if (i < lp && c < n16 && ((pmt >> pl) & 1u)) vt[i] = *reinterpret_cast<const uint4*>(baseT + off);
         }
+      };
+      auto fill_store = [&](int n16, uint32_t pm, uint32_t pmt, const uint4 (&va)[4], const uint4 (&vt)[4]) {
+        const int lg = n16 > 2 ? 2 : n16 - 1, lp = 1 << lg;
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -685,6 +689,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           if (i < lp && c < n16 && ((pmt >> pl) & 1u)) *reinterpret_cast<uint4*>(ST + pl * 80 + c * 16) = vt[i];
         }
         __syncwarp();
+      };
+      auto stage_fill2 = [&](const __half* baseA, const __half* baseT, int n16, uint32_t pm, uint32_t pmt,
+                             const __half* baseA1 = nullptr, uint32_t sel = 0u) {
+        uint4 va[4], vt[4];
+        fill_issue(baseA, baseT, n16, pm, pmt, baseA1, sel, va, vt);
+        fill_store(n16, pm, pmt, va, vt);
       };
       const uint32_t actm = __ballot_sync(0xffffffffu, act);
       const long long chan0 = cb0 + c_lo;       // my first channel in the row
@@ -771,10 +781,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         const bool known_upd = first || eps < 0.f;   // this pixel surely updates: x^T := 0 by bit 0
         const uint32_t tw = known_upd ? 0u : actm;   // x^T + dx rows to write
         float mx = 0.f;
+        uint4 nva[4], nvt[4];                    // the next slice's cache rows, loads in flight
 #pragma unroll 1
         for (int sl = 0; sl < C; sl += 32) {
           const int n16 = n16_of(sl);
-          if (sl > 0 && need_cache_w && actm) stage_fill2(gA + sl, gT + sl, n16, actm, tm, gA2 + sl, selm);
+          const bool nxt = sl + 32 < C && need_cache_w && actm;
+          if (nxt) fill_issue(gA + sl + 32, gT + sl + 32, n16_of(sl + 32), actm, tm, gA2 + sl + 32, selm, nva, nvt);
 #pragma unroll 1
           for (int c0 = sl; c0 < C && c0 < sl + 32; c0 += 8) {
             float z[8], a[8], t[8];
@@ -807,6 +819,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             stage_move(SD, gD + sl, n16, actm, 1);
             if (tw) stage_move(ST, gT + sl, n16, tw, 1);
           }
+          if (nxt) fill_store(n16_of(sl + 32), actm, tm, nva, nvt);
           TCTR(tid == 0 && u == 0 && sl == 0, 20);
         }
         TCTR(tid == 0 && u == 0, 15);
