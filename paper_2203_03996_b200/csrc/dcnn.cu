@@ -233,6 +233,7 @@ static bool plan_tc(Op& o, int dtype, int flags) {
   static const bool swz_only = getenv("DCNN_TC_SWZ_ONLY") != nullptr;
   static const bool swz_pad = getenv("DCNN_TC_SWZ_PAD") != nullptr;
   static const bool old_model = getenv("DCNN_TC_MODEL_OLD") != nullptr;
+  static const bool no_nab3 = getenv("DCNN_TC_NO_NAB3") != nullptr;   // A/B: the latency-regime rule below
   static const double t_req = getenv("DCNN_TC_TREQ") ? atof(getenv("DCNN_TC_TREQ")) : 0.0028;
   int WQs = p.WQ;
   if (swz_pad) while ((s * WQs) % 8) ++WQs;
@@ -278,6 +279,11 @@ static bool plan_tc(Op& o, int dtype, int flags) {
           for (int nab = 2; nab <= 4; ++nab) {
             if (nab > 2 && nab > ncb) break;
             if (force_nab && nab != std::min(force_nab, std::max(2, ncb))) continue;
+            // fewer than 4 streams (one-tile-per-CTA latency regime): 3 halo buffers wherever a
+            // tile has >= 3 channel blocks (same-box A/B: HRNet S = 1 +2.7 %, YOLOv5s S = 1 +0.5 %;
+            // at 8 streams it costs 1.5 %, profiles/r02_ab_env.txt)
+            // (a preference, not a constraint: a plan that only fits with other ring depths stays)
+            const double pref = (!force_nab && !no_nab3 && o.tS < 4 && ncb >= 3 && nab != 3) ? 1e6 : 0.0;
             // stride 2 with several streams: a halo block is 16-byte-TMA-request bound (~1.3 ns
             // each; 1188 for 16 channels of a 3x3 s2 tile), so keep >= 2 blocks in flight
             // (YOLOv5s 40x40x256 s2: K loop 79 -> 51 us, profiles/r02_trace_s2_convs_nab.txt;
@@ -305,7 +311,7 @@ static bool plan_tc(Op& o, int dtype, int flags) {
               t_w = nsteps * std::max(m_step, copy);
             }
             const double t_tile = std::max(std::max(t_halo, t_w), t_mmas);
-            const double cost = t_tile + t_epi + (waves - 1) * std::max(t_tile, t_epi);
+            const double cost = t_tile + t_epi + (waves - 1) * std::max(t_tile, t_epi) + pref;
             if (cost < best.cost - 1e-9) best = {cost, ns, BK, tg, stages, nab, resident, swzb};
           }
           if (resident) break;                            // resident: largest tg with <= 16 steps
