@@ -1081,8 +1081,12 @@ static dcnn_status create_impl(const dcnn_net_desc* d, dcnn_net* n) {
         o.grid_tc = ncl * p.nsplit;
 
         // a2 as a separate compaction kernel when the CTAs' scouts would otherwise walk many
-        // (mostly empty) tiles each: more than two tiles per cluster
-        o.scan = !force_fused && o.tS * o.nty * o.ntx > 2 * ncl;
+        // (mostly empty) tiles each: at least four tiles per cluster
+        // (at >= 4 tiles per cluster: same-box A/B, YOLOv5s S = 8 +4.0 % over a threshold of 2 --
+        // its 80x80 layers, ~2.7 tiles per CTA, run faster on the in-kernel scouts; the 160^2 and
+        // 320^2 layers, mostly inactive tiles, keep the compacted list; profiles/r02_ab_scanmin.txt)
+        static const int scan_min = getenv("DCNN_TC_SCAN_MIN") ? atoi(getenv("DCNN_TC_SCAN_MIN")) : 4;
+        o.scan = !force_fused && o.tS * o.nty * o.ntx > scan_min * ncl;
         static const bool show_plan = getenv("DCNN_TC_PLAN") != nullptr;
         if (show_plan)
           fprintf(stderr,
